@@ -1,0 +1,151 @@
+/*
+ * legpcg_b200 -- C ABI of the B200-native (sm_100a, fp64) hot path of the
+ * preconditioned Legendre-Galerkin PCG solver (arXiv:2004.13961).
+ *
+ * The reference (/root/reference/pkg, Python package `legpcg`) has no FFI;
+ * its boundary is the Python module API that `pcg_solve` calls.  Each entry
+ * point below replaces one reference function and cites it (file:line
+ * relative to /root/reference).  The Python shim `paper_2004_13961_b200`
+ * binds these with ctypes and re-exports the reference names.
+ *
+ * Conventions
+ *  - Plain C types only.  Handles are opaque, library-owned objects.
+ *  - Vectors are caller-owned DEVICE pointers, x-fastest ("Fortran") order,
+ *    exactly the PCG vectors of pcg.py:132-135.  Arrays documented as
+ *    "host or device" are copied with cudaMemcpyDefault (UVA).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *  - Every call returns 0 on success or a negative LP_ERR_* code;
+ *    lp_last_error() returns a human-readable message for the calling thread.
+ *  - Not thread-safe per handle: one handle per stream.
+ */
+#ifndef LEGPCG_B200_H
+#define LEGPCG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    LP_OK = 0,
+    LP_ERR_CUDA = -1,          /* CUDA runtime error (message in lp_last_error) */
+    LP_ERR_ARG = -2,           /* bad size / shape      -> ValueError            */
+    LP_ERR_NONPOSITIVE = -3,   /* beta <= 0 on the grid -> ValueError (operator.py:116-119) */
+    LP_ERR_ZERO_PIVOT = -4,    /* ILU(0) pivot          -> IluZeroPivotError (sparse.py:30-35) */
+    LP_ERR_INDEFINITE = -5,    /* p'Ap <= 0             -> IndefiniteOperatorError (pcg.py:34-42) */
+    LP_ERR_NODEVICE = -6,      /* no sm_100 device      -> RuntimeError          */
+    LP_ERR_OOM = -7            /* device allocation failed                        */
+};
+
+typedef struct lp_plan lp_plan;         /* TransformPlan (transforms.py:289-325)     */
+typedef struct lp_operator lp_operator; /* ProblemSpec + plan bound for A+B          */
+typedef struct lp_ilu lp_ilu;           /* SparseMatrix M and/or IluFactors          */
+
+const char *lp_last_error(void);
+const char *lp_version(void);
+/* Checks that device `device` is an sm_100 part and makes it current. */
+int lp_init(int device);
+
+/* ---------------------------------------------------------------- plans --
+ * TransformPlan(order, "reference") (transforms.py:298-310).  nodes/weights
+ * are the P-point Gauss rule (legendre.py:109-145) computed on the host, host
+ * or device pointers.  The library builds, on the device, the Vandermonde
+ * table V[k,n] = L_n(x_k) with the reference's recurrence (legendre.py:86-95)
+ * evaluated with separately rounded operations (bit-identical to the
+ * reference table), the Shen-basis tables Phi[k,m] = phi_m(x_k),
+ * dPhi[k,m] = phi_m'(x_k) (m < K = P-2), and their parity-split
+ * unfold/fold forms. */
+int lp_plan_create(int P, const double *nodes, const double *weights, lp_plan **out);
+int lp_plan_destroy(lp_plan *plan);
+/* Copies the P x P table V (row-major, V[k*P+n]) to `dst` (host or device). */
+int lp_plan_table(const lp_plan *plan, double *dst);
+
+/* tensor_bdlt / tensor_fdlt (transforms.py:368-375) of a P^d tensor.  The
+ * transform is applied to every axis; in/out are device, length P^d, any
+ * axis order (all axes are transformed identically). */
+int lp_tensor_bdlt(lp_plan *plan, int d, const double *in, double *out, void *stream);
+int lp_tensor_fdlt(lp_plan *plan, int d, const double *in, double *out, void *stream);
+
+/* ------------------------------------------------------------ operator --
+ * apply_A / apply_B / apply_system (operator.py:161-210).
+ * beta_grid: P^d values of beta on the Gauss grid, x fastest (host or
+ *   device), used when n_axis_betas == 0;
+ * axis_betas: n_axis_betas == d arrays of P values beta_i(x_i) for the
+ *   per-axis diffusion form (operator.py:155-158);
+ * alpha_grid: P^d values of alpha, or NULL when alpha is None / is_zero.
+ * The positivity test of operator.py:116-119 runs once, at creation. */
+int lp_operator_create(lp_plan *plan, int d, const double *beta_grid,
+                       int n_axis_betas, const double *const *axis_betas,
+                       const double *alpha_grid, lp_operator **out);
+int lp_operator_destroy(lp_operator *op);
+/* which: 1 = A (apply_A), 2 = B (apply_B), 3 = A + B (apply_system).
+ * u, out: device, K^d, x fastest.  out may not alias u. */
+int lp_apply(lp_operator *op, int which, const double *u, double *out, void *stream);
+
+/* ----------------------------------------------------- preconditioner --
+ * General CSR matrix (SparseMatrix, sparse.py:38-86): upload and hold.
+ * indptr[n+1], indices[nnz] (sorted per row), values[nnz]; host or device. */
+int lp_csr_create(int64_t n, int64_t nnz, const int64_t *indptr,
+                  const int32_t *indices, const double *values, lp_ilu **out);
+
+/* assemble_M (precond.py:207-297) into the implicit-offset "box" layout:
+ * M[row][slot], slot <-> offset (o_x, o_y, o_z) in [-r, r]^d, x fastest.
+ * n_groups terms; group g has a hat tensor of shape lens[g][0..d-1]
+ * (C order, axis 0 = x), stiff_axis[g] in {-1, 0..d-1}.  The 1-D blocks
+ * S^(t), M^(t) (building_blocks_1d, precond.py:118-161) are passed as
+ * diagonal stacks: blocks[kind][t][o + R][i] = entry (i, i+o) of block t
+ * (kind 0 = stiff, 1 = mass), for t <= tmax, |o| <= R = tmax + 2, i < K.
+ * Entries |v| < 1e-300 are dropped from the pattern (precond.py:272-297). */
+int lp_box_assemble(int d, int K, int n_groups, const int *lens,
+                    const int *stiff_axis, const double *const *hats,
+                    int tmax, const double *blocks, lp_ilu **out);
+
+/* Number of stored entries (SparseMatrix.nnz) and CSR export (host arrays
+ * sized by nnz; indices/values may be NULL to fetch only indptr). */
+int lp_matrix_nnz(const lp_ilu *m, int64_t *nnz);
+int lp_matrix_export(const lp_ilu *m, int which /*0=M,1=L,2=U*/, int64_t *indptr,
+                     int32_t *indices, double *values);
+
+/* ilu0 (sparse.py:142-172): factor in place, keeping the original M.  On a
+ * zero pivot returns LP_ERR_ZERO_PIVOT with *bad_row set to the row the
+ * reference would report (missing diagonal, |u_kk| < pivot_tol). */
+int lp_ilu0(lp_ilu *m, double pivot_tol, int64_t *bad_row, void *stream);
+
+/* forward_sub / backward_sub / precond_apply (sparse.py:199-221). */
+int lp_forward_sub(lp_ilu *f, const double *r, double *y, void *stream);
+int lp_backward_sub(lp_ilu *f, const double *y, double *z, void *stream);
+int lp_precond_apply(lp_ilu *f, const double *r, double *z, void *stream);
+/* y = M x with the ORIGINAL matrix (spmv, sparse.py:97-113). */
+int lp_spmv(lp_ilu *m, const double *x, double *y, void *stream);
+int lp_ilu_destroy(lp_ilu *m);
+
+/* ------------------------------------------------------------------ PCG --
+ * pcg_solve loop (pcg.py:111-179): x (device, n) holds x0 on entry when
+ * has_x0 != 0 and the solution on exit.  precond may be NULL (plain CG).
+ * history (host, k_max + 1 doubles, may be NULL) receives ||r_k||_2.
+ * Dots are deterministic double-double reductions (the reference accumulates
+ * in 80-bit long double, pcg.py:77-79). */
+typedef struct lp_report {
+    int64_t iterations;
+    int32_t converged;
+    int32_t pad_;
+    double final_relative_residual;
+    double loop_seconds;
+    double indefinite_value;   /* p'Ap at the failing iteration */
+    int64_t kernel_launches;   /* this library's kernels launched by the loop */
+} lp_report;
+
+int lp_pcg_solve(lp_operator *op, lp_ilu *precond, const double *F, double *x,
+                 int has_x0, double epsilon, int64_t k_max, double *history,
+                 lp_report *report, void *stream);
+
+/* --------------------------------------------------------- vector ops --
+ * Building blocks exposed for tests and for host-driven loops. */
+/* out[0..1] (device) = double-double sum_i a_i b_i, deterministic order. */
+int lp_dot(int64_t n, const double *a, const double *b, double *out2, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEGPCG_B200_H */

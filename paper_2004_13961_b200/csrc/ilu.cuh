@@ -1,0 +1,56 @@
+// Internal definition of the sparse-matrix / ILU(0) handle.
+#pragma once
+
+#include "lp_common.cuh"
+
+namespace lp {
+
+enum { MAT_CSR = 0, MAT_BOX = 1 };
+
+// Implicit-offset ("box") storage of a Kronecker-banded matrix: every row has
+// S = (2r+1)^d slots, slot s <-> offset (ox, oy, oz) in [-r, r]^d with ox
+// fastest; values[row * S + s] holds entry (row, row + ox + K oy + K^2 oz) or
+// 0 where that column is outside the grid.  Slot order equals column order for
+// the valid slots of every row (|ox| < K), so "lower" = s < S/2, "diag" = S/2.
+struct BoxLayout {
+    int d = 0, K = 0, r = 0, W = 0;   // W = 2r + 1
+    int S = 0;                        // W^d slots
+    int64_t n = 0;
+    double *values = nullptr;         // original M            [n][S]
+    double *lu = nullptr;             // ILU(0) factors         [n][S]
+    uint32_t *mask = nullptr;         // in-pattern bits        [n][ceil(S/32)] (null: all valid slots)
+    int mask_words = 0;
+    int64_t nnz = 0;
+};
+
+}  // namespace lp
+
+struct lp_ilu {
+    int kind = lp::MAT_CSR;
+    int64_t n = 0, nnz = 0;
+    // CSR (kind == MAT_CSR)
+    int64_t *indptr = nullptr;
+    int32_t *indices = nullptr;
+    double *values = nullptr;   // original M
+    double *lu = nullptr;       // factors in the pattern of M (L strictly lower, U upper)
+    int64_t *diag = nullptr;
+    // box layout (kind == MAT_BOX)
+    lp::BoxLayout box;
+    // sweep state
+    bool factored = false;
+    int *flags = nullptr;       // per-row progress, compared against `epoch`
+    int epoch = 0;
+    int *ticket = nullptr;      // dynamic row tickets (2 counters)
+    int64_t *bad = nullptr;     // zero-pivot key (device)
+    double *ytmp = nullptr;     // forward-sweep result for precond_apply
+    int64_t missing_diag = -1;  // first row without a stored diagonal (box assembly)
+};
+
+namespace lp {
+int ilu_apply(lp_ilu *m, const double *r, double *z, cudaStream_t st);
+int box_forward(lp_ilu *m, const double *r, double *y, cudaStream_t st);
+int box_backward(lp_ilu *m, const double *y, double *z, cudaStream_t st);
+int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st);
+int box_spmv(lp_ilu *m, const double *x, double *y, cudaStream_t st);
+int box_export(const lp_ilu *m, int which, int64_t *indptr, int32_t *indices, double *values);
+}  // namespace lp

@@ -1,0 +1,664 @@
+// Kronecker-banded preconditioner M in the implicit-offset "box" layout:
+// assembly, ILU(0) factorisation, forward/backward sweeps, SpMV, export.
+//
+// Reference: precond.py:207-297 (assemble_M, _symmetrize, _compress),
+// sparse.py:116-221 (ilu0, forward_sub, backward_sub, precond_apply).
+//
+// Layout: values[row][slot], row = ix + K (iy + K iz) (x fastest, the CSR row
+// order of precond.py:275-285), slot s <-> offset (ox, oy, oz) in [-r, r]^d,
+// s = (ox+r) + W ((oy+r) + W (oz+r)).  No column indices are stored.  For the
+// valid slots of a row, slot order is column order, so the reference's
+// "k < i in increasing column order" is "s < c in increasing slot order",
+// c = (S-1)/2 the diagonal.  An in-pattern bit per (row, slot) reproduces the
+// reference's stored pattern (valid column and |m| >= 1e-300); out-of-pattern
+// values are exactly zero.
+#include <math.h>
+
+#include <vector>
+
+#include "ilu.cuh"
+
+namespace lp {
+namespace {
+
+struct Geom {
+    int d, K, r, W, S, c, mw;   // mw = mask words per row
+    int64_t n;
+    int nlines;
+};
+
+Geom geom_of(const BoxLayout &b) {
+    Geom g;
+    g.d = b.d;
+    g.K = b.K;
+    g.r = b.r;
+    g.W = b.W;
+    g.S = b.S;
+    g.c = (b.S - 1) / 2;
+    g.mw = b.mask_words;
+    g.n = b.n;
+    g.nlines = (int)(b.n / b.K);
+    return g;
+}
+
+__device__ __forceinline__ void slot_axes(const Geom &g, int s, int &sx, int &sy, int &sz) {
+    sx = s % g.W;
+    const int q = s / g.W;
+    sy = g.d > 1 ? q % g.W : g.r;
+    sz = g.d > 2 ? q / g.W : g.r;
+}
+
+__device__ __forceinline__ void row_pos(const Geom &g, int64_t i, int &ix, int &iy, int &iz) {
+    ix = (int)(i % g.K);
+    const int64_t q = i / g.K;
+    iy = g.d > 1 ? (int)(q % g.K) : 0;
+    iz = g.d > 2 ? (int)(q / g.K) : 0;
+}
+
+// Column of slot s for row i, or -1 if it leaves the grid.
+__device__ __forceinline__ int64_t slot_col(const Geom &g, int64_t i, int ix, int iy, int iz,
+                                            int s) {
+    int sx, sy, sz;
+    slot_axes(g, s, sx, sy, sz);
+    const int ox = sx - g.r, oy = sy - g.r, oz = sz - g.r;
+    if (ix + ox < 0 || ix + ox >= g.K) return -1;
+    if (g.d > 1 && (iy + oy < 0 || iy + oy >= g.K)) return -1;
+    if (g.d > 2 && (iz + oz < 0 || iz + oz >= g.K)) return -1;
+    return i + ox + (int64_t)g.K * (oy + (int64_t)g.K * oz);
+}
+
+// ----------------------------------------------------------------- assembly
+
+struct GroupDesc {
+    int lens[3];
+    int kind[3];       // 0 = stiff block, 1 = mass block, per axis
+    int64_t hat_off;   // offset into the concatenated hat array
+};
+
+struct AsmArgs {
+    Geom g;
+    int ngroups, tmax, R;
+    GroupDesc grp[4];
+    const double *hats;
+    const double *blocks;   // [2][tmax+1][2R+1][K]
+};
+
+__device__ __forceinline__ double blk(const AsmArgs &a, int kind, int t, int o, int i) {
+    return __ldg(a.blocks + (((size_t)kind * (a.tmax + 1) + t) * (2 * a.R + 1) + (o + a.R)) * a.g.K + i);
+}
+
+// One CTA per (line, slot-line): H_g[a] = sum_{b,c} hat_g[a,b,c] Y_b[oy](iy) Z_c[oz](iz)
+// over parity-matched degrees, then raw(ix, ox) = sum_g sum_a H_g[a] X_a[ox](ix).
+__global__ void box_raw_kernel(const __grid_constant__ AsmArgs a, double *__restrict__ vals) {
+    const Geom &g = a.g;
+    __shared__ double H[4][64];
+    const int line = blockIdx.x, sl = blockIdx.y;
+    const int iy = g.d > 1 ? line % g.K : 0, iz = g.d > 2 ? line / g.K : 0;
+    const int oy = g.d > 1 ? sl % g.W - g.r : 0, oz = g.d > 2 ? sl / g.W - g.r : 0;
+    for (int q = threadIdx.x; q < a.ngroups * 64; q += blockDim.x) {
+        const int gi = q / 64, ax = q % 64;
+        const GroupDesc &G = a.grp[gi];
+        if (ax >= G.lens[0]) continue;
+        double h = 0.0;
+        const int ly = G.lens[1], lz = G.lens[2];
+        for (int b = (oy & 1); b < ly; b += 2) {
+            const double yb = g.d > 1 ? blk(a, G.kind[1], b, oy, iy) : 1.0;
+            for (int c = (oz & 1); c < lz; c += 2) {
+                const double zc = g.d > 2 ? blk(a, G.kind[2], c, oz, iz) : 1.0;
+                h += a.hats[G.hat_off + ((size_t)ax * ly + b) * lz + c] * yb * zc;
+            }
+        }
+        H[gi][ax] = h;
+    }
+    __syncthreads();
+    const int64_t rowbase = (int64_t)line * g.K;
+    const int sbase = g.W * sl;
+    for (int q = threadIdx.x; q < g.K * g.W; q += blockDim.x) {
+        const int ix = q / g.W, sx = q % g.W, ox = sx - g.r;
+        double v = 0.0;
+        for (int gi = 0; gi < a.ngroups; ++gi) {
+            const GroupDesc &G = a.grp[gi];
+            for (int t = (ox & 1); t < G.lens[0]; t += 2) v += H[gi][t] * blk(a, G.kind[0], t, ox, ix);
+        }
+        vals[(rowbase + ix) * g.S + sbase + sx] = v;
+    }
+}
+
+// Average every lower entry with its transpose (precond.py:255-269).
+__global__ void box_sym_kernel(Geom g, double *vals) {
+    const int64_t total = g.n * g.c;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = q / g.c;
+        const int s = (int)(q % g.c);
+        int ix, iy, iz;
+        row_pos(g, i, ix, iy, iz);
+        const int64_t j = slot_col(g, i, ix, iy, iz, s);
+        if (j < 0) continue;
+        const size_t a = (size_t)i * g.S + s, b = (size_t)j * g.S + (g.S - 1 - s);
+        const double avg = 0.5 * (vals[a] + vals[b]);
+        vals[a] = avg;
+        vals[b] = avg;
+    }
+}
+
+// Pattern bits (valid column and |v| >= 1e-300, precond.py:281), zero the rest,
+// count nnz, flag rows whose diagonal is not stored.
+__global__ void box_mask_kernel(Geom g, double *vals, uint32_t *mask,
+                                unsigned long long *nnz, unsigned long long *missing) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    unsigned long long cnt = 0;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < g.n * g.mw;
+         w += nwarps) {
+        const int64_t i = w / g.mw;
+        const int word = (int)(w % g.mw);
+        const int s = word * 32 + lane;
+        bool in = false;
+        if (s < g.S) {
+            int ix, iy, iz;
+            row_pos(g, i, ix, iy, iz);
+            double *p = vals + (size_t)i * g.S + s;
+            in = slot_col(g, i, ix, iy, iz, s) >= 0 && fabs(*p) >= 1e-300;
+            if (!in) *p = 0.0;
+            if (s == g.c && !in) atomicMin(missing, (unsigned long long)i);
+        }
+        const unsigned bits = __ballot_sync(0xffffffff, in);
+        if (lane == 0) {
+            mask[(size_t)i * g.mw + word] = bits;
+            cnt += __popc(bits);
+        }
+    }
+    if (lane == 0 && cnt) atomicAdd(nnz, cnt);
+}
+
+// ----------------------------------------------------------- factorisation
+//
+// IKJ ILU(0) (sparse.py:116-139) with one CTA per row, rows handed out in
+// natural order by a ticket.  Row i lives in shared memory; for every lower
+// in-pattern slot s (ascending = column order) the CTA waits for row
+// k = i + off(s) to be final, forms l = a_is / u_kk, and applies
+// a_it -= l u_ks' for every upper slot s' of row k whose target offset
+// off(s) + off(s') is an in-pattern slot t of row i.  Updates of one step hit
+// distinct targets; steps are separated by a barrier, so each entry receives
+// its updates in the reference's k order, each as a separately rounded
+// multiply and subtract: the factors are bit-identical to the reference's for
+// the same M.
+
+template <int TPR>
+__device__ __forceinline__ void row_sync() {
+    if (TPR == 32) __syncwarp();
+    else __syncthreads();
+}
+
+template <int TPR>
+__global__ void __launch_bounds__(TPR)
+box_ilu0_kernel(Geom g, double *lu, const uint32_t *__restrict__ mask, int *flags, int epoch,
+                int *ticket, double tol, unsigned long long *bad) {
+    extern __shared__ __align__(16) double sm[];
+    double *row = sm;                     // [S]
+    double *lval = sm + g.S;              // [c]
+    uint32_t *bits = reinterpret_cast<uint32_t *>(lval + g.c);   // [mw]
+    __shared__ int64_t sh_row;
+    const int tid = threadIdx.x;
+    for (;;) {
+        if (tid == 0) sh_row = atomicAdd(ticket, 1);
+        row_sync<TPR>();
+        const int64_t i = sh_row;
+        if (i >= g.n) return;
+        int ix, iy, iz;
+        row_pos(g, i, ix, iy, iz);
+        for (int s = tid; s < g.S; s += TPR) {
+            const double v = lu[(size_t)i * g.S + s];
+            row[s] = v;
+            if (s < g.c) lval[s] = v;
+        }
+        for (int w = tid; w < g.mw; w += TPR) bits[w] = mask[(size_t)i * g.mw + w];
+        row_sync<TPR>();
+        for (int s = 0; s < g.c; ++s) {
+            if (!((bits[s >> 5] >> (s & 31)) & 1u)) continue;
+            int sx, sy, sz;
+            slot_axes(g, s, sx, sy, sz);
+            const int64_t k = i + (sx - g.r) + (int64_t)g.K * ((sy - g.r) + (int64_t)g.K * (sz - g.r));
+            if (tid == 0) {
+                const volatile int *f = flags + k;
+                while (*f != epoch) {
+                }
+                __threadfence();
+            }
+            row_sync<TPR>();
+            const double *uk = lu + (size_t)k * g.S;
+            const double piv = __ldcg(uk + g.c);
+            const double l = __ddiv_rn(row[s], piv);
+            if (tid == 0) {
+                lval[s] = l;
+                if (fabs(piv) < tol) atomicMin(bad, (unsigned long long)(i * g.n + k));
+            }
+            // row k position and the sub-box of upper slots s' whose target stays in the box
+            const int kx = ix + sx - g.r, ky = iy + sy - g.r, kz = iz + sz - g.r;
+            const int xlo = max(g.r - sx, 0), xhi = min(g.W + g.r - sx, g.W);
+            // the most significant axis of an upper slot is >= r; the others span their range
+            const int ylo = g.d > 1 ? max(g.r - sy, g.d == 2 ? g.r : 0) : 0;
+            const int yhi = g.d > 1 ? min(g.W + g.r - sy, g.W) : 1;
+            const int zlo = g.d > 2 ? max(g.r - sz, g.r) : 0, zhi = g.d > 2 ? min(g.W + g.r - sz, g.W) : 1;
+            // threads: lane along x, the rest along (y, z) pairs
+            const int nx = xhi - xlo;
+            const int lanes_x = 32;
+            const int tx = tid % lanes_x, tyz = tid / lanes_x, nyz_threads = TPR / lanes_x;
+            const int ny = yhi - ylo, nz = zhi - zlo;
+            const int sxp = xlo + tx;
+            if (tx < nx) {
+                const int colx = kx + sxp - g.r;
+                const bool xok = colx >= 0 && colx < g.K;
+                for (int q = tyz; q < ny * nz; q += nyz_threads) {
+                    const int syp = g.d > 1 ? ylo + q % ny : g.r;
+                    const int szp = g.d > 2 ? zlo + q / ny : g.r;
+                    const int sp = sxp + g.W * (syp + g.W * szp);
+                    if (sp <= g.c || !xok) continue;
+                    if (g.d > 1) {
+                        const int cy = ky + syp - g.r;
+                        if (cy < 0 || cy >= g.K) continue;
+                    }
+                    if (g.d > 2) {
+                        const int cz = kz + szp - g.r;
+                        if (cz < 0 || cz >= g.K) continue;
+                    }
+                    const int t = (sx + sxp - g.r) + g.W * ((sy + syp - g.r) + g.W * (sz + szp - g.r));
+                    if (!((bits[t >> 5] >> (t & 31)) & 1u)) continue;
+                    row[t] = __dsub_rn(row[t], __dmul_rn(l, __ldcg(uk + sp)));
+                }
+            }
+            row_sync<TPR>();
+        }
+        for (int s = tid; s < g.S; s += TPR) __stcg(lu + (size_t)i * g.S + s, s < g.c ? lval[s] : row[s]);
+        __threadfence();
+        row_sync<TPR>();
+        if (tid == 0) {
+            __threadfence();
+            *((volatile int *)(flags + i)) = epoch;
+        }
+    }
+}
+
+// ------------------------------------------------------------------- sweeps
+//
+// Warp per x-line, lines handed out in natural (reverse) order by a ticket;
+// rows of a line are swept in order by the warp.  Row (ix, line) needs the
+// rows ix' <= ix + r of every earlier line in its stencil; by induction it
+// suffices to wait on the previous line of the same plane and on line
+// (min(iy + r, K-1), iz - 1) of the previous plane.  Per-line progress
+// counters are 64-bit: epoch * (K + 1) + rows done.
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+    return v;
+}
+
+__device__ __forceinline__ void wait_progress(const long long *prog, int line, long long need,
+                                              long long &seen) {
+    if (line < 0 || seen >= need) return;
+    const volatile long long *p = prog + line;
+    long long v;
+    while ((v = *p) < need) {
+    }
+    seen = v;
+    __threadfence();
+}
+
+__global__ void box_fwd_kernel(Geom g, const double *__restrict__ lu, const double *__restrict__ rhs,
+                               double *y, long long *prog, long long base, int *ticket) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        int L = 0;
+        if (lane == 0) L = atomicAdd(ticket, 1);
+        L = __shfl_sync(0xffffffff, L, 0);
+        if (L >= g.nlines) return;
+        const int iy = g.d > 1 ? L % g.K : 0, iz = g.d > 2 ? L / g.K : 0;
+        const int dep1 = (g.d > 1 && iy > 0) ? L - 1 : -1;
+        const int dep2 = (g.d > 2 && iz > 0) ? min(iy + g.r, g.K - 1) + g.K * (iz - 1) : -1;
+        long long seen1 = -1, seen2 = -1;
+        for (int ix = 0; ix < g.K; ++ix) {
+            if (lane == 0) {
+                const long long need = base + min(g.K, ix + g.r + 1);
+                wait_progress(prog, dep1, need, seen1);
+                wait_progress(prog, dep2, need, seen2);
+            }
+            __syncwarp();
+            const int64_t i = (int64_t)L * g.K + ix;
+            const double *lr = lu + (size_t)i * g.S;
+            double acc = 0.0;
+            for (int s = lane; s < g.c; s += 32) {
+                const double v = __ldg(lr + s);
+                if (v != 0.0) {
+                    const int64_t col = slot_col(g, i, ix, iy, iz, s);
+                    acc = fma(v, __ldcg(y + col), acc);
+                }
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) {
+                __stcg(y + i, rhs[i] - acc);
+                __threadfence();
+                *((volatile long long *)(prog + L)) = base + ix + 1;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+__global__ void box_bwd_kernel(Geom g, const double *__restrict__ lu, const double *__restrict__ rhs,
+                               double *z, long long *prog, long long base, int *ticket) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(ticket, 1);
+        t = __shfl_sync(0xffffffff, t, 0);
+        if (t >= g.nlines) return;
+        const int L = g.nlines - 1 - t;
+        const int iy = g.d > 1 ? L % g.K : 0, iz = g.d > 2 ? L / g.K : 0;
+        const int dep1 = (g.d > 1 && iy < g.K - 1) ? L + 1 : -1;
+        const int dep2 = (g.d > 2 && iz < g.K - 1) ? max(iy - g.r, 0) + g.K * (iz + 1) : -1;
+        long long seen1 = -1, seen2 = -1;
+        for (int ix = g.K - 1; ix >= 0; --ix) {
+            if (lane == 0) {
+                const long long need = base + min(g.K, g.K - ix + g.r);
+                wait_progress(prog, dep1, need, seen1);
+                wait_progress(prog, dep2, need, seen2);
+            }
+            __syncwarp();
+            const int64_t i = (int64_t)L * g.K + ix;
+            const double *ur = lu + (size_t)i * g.S;
+            double acc = 0.0;
+            for (int s = g.c + 1 + lane; s < g.S; s += 32) {
+                const double v = __ldg(ur + s);
+                if (v != 0.0) {
+                    const int64_t col = slot_col(g, i, ix, iy, iz, s);
+                    acc = fma(v, __ldcg(z + col), acc);
+                }
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) {
+                __stcg(z + i, (rhs[i] - acc) / __ldg(ur + g.c));
+                __threadfence();
+                *((volatile long long *)(prog + L)) = base + (g.K - ix);
+            }
+            __syncwarp();
+        }
+    }
+}
+
+__global__ void box_spmv_kernel(Geom g, const double *__restrict__ vals, const double *__restrict__ x,
+                                double *__restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (i >= g.n) return;
+    int ix, iy, iz;
+    row_pos(g, i, ix, iy, iz);
+    double acc = 0.0;
+    for (int s = lane; s < g.S; s += 32) {
+        const double v = vals[(size_t)i * g.S + s];
+        if (v != 0.0) acc = fma(v, x[slot_col(g, i, ix, iy, iz, s)], acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) y[i] = acc;
+}
+
+constexpr int SWEEP_WARPS = 4;
+
+unsigned sweep_blocks(int nlines) {
+    const int cap = 148 * 16;
+    const int b = (nlines + SWEEP_WARPS - 1) / SWEEP_WARPS;
+    return (unsigned)(b < cap ? b : cap);
+}
+
+}  // namespace
+
+// progress counters live in the generic `flags` buffer of the handle (sized for n ints,
+// which is >= 2 * nlines ints for K >= 2)
+static long long *box_prog(lp_ilu *m) { return reinterpret_cast<long long *>(m->flags); }
+
+int box_forward(lp_ilu *m, const double *r, double *y, cudaStream_t st) {
+    Geom g = geom_of(m->box);
+    const long long base = (long long)(++m->epoch) * (g.K + 1);
+    LP_CUDA(cudaMemsetAsync(m->ticket, 0, sizeof(int), st));
+    box_fwd_kernel<<<sweep_blocks(g.nlines), 32 * SWEEP_WARPS, 0, st>>>(
+        g, m->box.lu, r, y, box_prog(m), base, m->ticket);
+    count_launch();
+    LP_CHECK_LAUNCH();
+    return LP_OK;
+}
+
+int box_backward(lp_ilu *m, const double *y, double *z, cudaStream_t st) {
+    Geom g = geom_of(m->box);
+    const long long base = (long long)(++m->epoch) * (g.K + 1);
+    LP_CUDA(cudaMemsetAsync(m->ticket, 0, sizeof(int), st));
+    box_bwd_kernel<<<sweep_blocks(g.nlines), 32 * SWEEP_WARPS, 0, st>>>(
+        g, m->box.lu, y, z, box_prog(m), base, m->ticket);
+    count_launch();
+    LP_CHECK_LAUNCH();
+    return LP_OK;
+}
+
+int box_spmv(lp_ilu *m, const double *x, double *y, cudaStream_t st) {
+    Geom g = geom_of(m->box);
+    LP_ARG(m->box.values != nullptr, "original matrix was released (factored in place)");
+    box_spmv_kernel<<<(unsigned)ceil_div(g.n * 32, 256), 256, 0, st>>>(g, m->box.values, x, y);
+    count_launch();
+    LP_CHECK_LAUNCH();
+    return LP_OK;
+}
+
+int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st) {
+    BoxLayout &b = m->box;
+    Geom g = geom_of(b);
+    if (m->missing_diag >= 0) {
+        *bad_row = m->missing_diag;
+        set_error("zero pivot at elimination step %lld", (long long)*bad_row);
+        return LP_ERR_ZERO_PIVOT;
+    }
+    const size_t bytes = (size_t)b.n * b.S * sizeof(double);
+    if (!b.lu) {
+        if (dalloc(&b.lu, (size_t)b.n * b.S, "ILU factors") != LP_OK) {
+            // not enough memory for a separate copy: factor in place, drop M
+            b.lu = b.values;
+            b.values = nullptr;
+        }
+    }
+    if (b.values) LP_CUDA(cudaMemcpyAsync(b.lu, b.values, bytes, cudaMemcpyDeviceToDevice, st));
+    else if (m->factored) {
+        set_error("matrix was factored in place; re-assemble before refactoring");
+        return LP_ERR_ARG;
+    }
+    unsigned long long *key = reinterpret_cast<unsigned long long *>(m->bad);
+    const unsigned long long none = ~0ull;
+    LP_CUDA(cudaMemcpyAsync(key, &none, sizeof none, cudaMemcpyHostToDevice, st));
+    // row flags: reuse `flags` as int per row (progress counters are re-based per sweep call)
+    LP_CUDA(cudaMemsetAsync(m->flags, 0, b.n * sizeof(int), st));
+    LP_CUDA(cudaMemsetAsync(m->ticket, 0, sizeof(int), st));
+    const int epoch = 1;
+    const size_t smem = (size_t)g.S * sizeof(double) + (size_t)g.c * sizeof(double) +
+                        (size_t)g.mw * sizeof(uint32_t) + 16;
+    int dev;
+    LP_CUDA(cudaGetDevice(&dev));
+    int nsm = 148;
+    LP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (g.S <= 1200) {
+        LP_CUDA(cudaFuncSetAttribute(box_ilu0_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        int occ = 1;
+        LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, box_ilu0_kernel<32>, 32, smem));
+        int64_t blocks = (int64_t)occ * nsm;
+        if (blocks > g.n) blocks = g.n;
+        box_ilu0_kernel<32><<<(unsigned)blocks, 32, smem, st>>>(g, b.lu, b.mask, m->flags, epoch,
+                                                               m->ticket, tol, key);
+    } else {
+        LP_CUDA(cudaFuncSetAttribute(box_ilu0_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        int occ = 1;
+        LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, box_ilu0_kernel<256>, 256, smem));
+        int64_t blocks = (int64_t)occ * nsm;
+        if (blocks > g.n) blocks = g.n;
+        box_ilu0_kernel<256><<<(unsigned)blocks, 256, smem, st>>>(g, b.lu, b.mask, m->flags, epoch,
+                                                                 m->ticket, tol, key);
+    }
+    count_launch();
+    LP_CHECK_LAUNCH();
+    unsigned long long hk;
+    double plast;
+    LP_CUDA(cudaMemcpyAsync(&hk, key, sizeof hk, cudaMemcpyDeviceToHost, st));
+    LP_CUDA(cudaMemcpyAsync(&plast, b.lu + (size_t)(b.n - 1) * b.S + g.c, sizeof plast,
+                            cudaMemcpyDeviceToHost, st));
+    LP_CUDA(cudaStreamSynchronize(st));
+    // progress counters for the sweeps start from a clean slate
+    LP_CUDA(cudaMemset(m->flags, 0, b.n * sizeof(int)));
+    m->epoch = 0;
+    if (hk != none) *bad_row = (int64_t)(hk % (unsigned long long)b.n);
+    else if (fabs(plast) < tol) *bad_row = b.n - 1;
+    if (*bad_row >= 0) {
+        set_error("zero pivot at elimination step %lld", (long long)*bad_row);
+        return LP_ERR_ZERO_PIVOT;
+    }
+    m->factored = true;
+    return LP_OK;
+}
+
+int box_export(const lp_ilu *m, int which, int64_t *indptr, int32_t *indices, double *values) {
+    const BoxLayout &b = m->box;
+    const double *src = which == 0 ? b.values : b.lu;
+    LP_ARG(src != nullptr, "original matrix was released (factored in place)");
+    Geom g = geom_of(b);
+    std::vector<uint32_t> mk((size_t)b.n * b.mask_words);
+    LP_CUDA(cudaMemcpy(mk.data(), b.mask, mk.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    const int64_t chunk = 1 << 14;
+    std::vector<double> buf;
+    int64_t out = 0;
+    indptr[0] = 0;
+    const int slo = which == 2 ? g.c : 0, shi = which == 1 ? g.c : g.S;
+    for (int64_t i0 = 0; i0 < b.n; i0 += chunk) {
+        const int64_t rows = (b.n - i0) < chunk ? (b.n - i0) : chunk;
+        if (values) {
+            buf.resize((size_t)rows * b.S);
+            LP_CUDA(cudaMemcpy(buf.data(), src + (size_t)i0 * b.S, buf.size() * sizeof(double),
+                               cudaMemcpyDeviceToHost));
+        }
+        for (int64_t i = i0; i < i0 + rows; ++i) {
+            for (int s = slo; s < shi; ++s) {
+                if (!((mk[(size_t)i * b.mask_words + (s >> 5)] >> (s & 31)) & 1u)) continue;
+                const int sx = s % g.W, qq = s / g.W;
+                const int sy = g.d > 1 ? qq % g.W : g.r, sz = g.d > 2 ? qq / g.W : g.r;
+                const int64_t col = i + (sx - g.r) + (int64_t)g.K * ((sy - g.r) + (int64_t)g.K * (sz - g.r));
+                if (indices) indices[out] = (int32_t)col;
+                if (values) values[out] = buf[(size_t)(i - i0) * b.S + s];
+                ++out;
+            }
+            indptr[i + 1] = out;
+        }
+    }
+    return LP_OK;
+}
+
+}  // namespace lp
+
+using namespace lp;
+
+extern "C" int lp_box_assemble(int d, int K, int n_groups, const int *lens, const int *stiff_axis,
+                               const double *const *hats, int tmax, const double *blocks,
+                               lp_ilu **out) {
+    *out = nullptr;
+    LP_ARG(d >= 1 && d <= 3, "dim must be 1, 2 or 3");
+    LP_ARG(K >= 1, "empty preconditioner: K = 0");
+    LP_ARG(n_groups >= 1 && n_groups <= 4, "1..4 coefficient groups supported");
+    LP_ARG(tmax >= 0 && tmax < 64, "truncation degree out of range");
+    AsmArgs a{};
+    a.ngroups = n_groups;
+    a.tmax = tmax;
+    a.R = tmax + 2;
+    int r = 0;
+    int64_t hat_total = 0;
+    for (int gi = 0; gi < n_groups; ++gi) {
+        GroupDesc &G = a.grp[gi];
+        int64_t cnt = 1;
+        for (int ax = 0; ax < 3; ++ax) {
+            G.lens[ax] = ax < d ? lens[gi * d + ax] : 1;
+            G.kind[ax] = (stiff_axis[gi] == ax) ? 0 : 1;
+            LP_ARG(G.lens[ax] >= 1 && G.lens[ax] <= tmax + 1, "hat extent out of range");
+            cnt *= G.lens[ax];
+            if (ax < d) {
+                const int reach = G.lens[ax] - 1 + (G.kind[ax] == 0 ? 0 : 2);
+                if (reach > r) r = reach;
+            }
+        }
+        G.hat_off = hat_total;
+        hat_total += cnt;
+    }
+    lp_ilu *m = new lp_ilu();
+    m->kind = MAT_BOX;
+    BoxLayout &b = m->box;
+    b.d = d;
+    b.K = K;
+    b.r = r;
+    b.W = 2 * r + 1;
+    b.S = b.W;
+    for (int ax = 1; ax < d; ++ax) b.S *= b.W;
+    b.n = K;
+    for (int ax = 1; ax < d; ++ax) b.n *= K;
+    b.mask_words = (b.S + 31) / 32;
+    m->n = b.n;
+    int rc;
+    double *dhats = nullptr, *dblocks = nullptr;
+    unsigned long long *cnt = nullptr;
+    const size_t nblk = (size_t)2 * (tmax + 1) * (2 * a.R + 1) * K;
+    auto fail = [&](int code) {
+        if (dhats) cudaFree(dhats);
+        if (dblocks) cudaFree(dblocks);
+        if (cnt) cudaFree(cnt);
+        lp_ilu_destroy(m);
+        return code;
+    };
+    if ((rc = dalloc(&b.values, (size_t)b.n * b.S, "preconditioner values")) ||
+        (rc = dalloc(&b.mask, (size_t)b.n * b.mask_words, "pattern bits")) ||
+        (rc = dalloc(&dhats, hat_total, "hats")) || (rc = dalloc(&dblocks, nblk, "1-D blocks")) ||
+        (rc = dalloc(&cnt, 2, "counters")) ||
+        (rc = dalloc(&m->flags, b.n > 2 * (b.n / K) + 2 ? b.n : 2 * (b.n / K) + 2, "flags")) ||
+        (rc = dalloc(&m->ticket, 4, "tickets")) || (rc = dalloc(&m->bad, 1, "pivot key")) ||
+        (rc = dalloc(&m->ytmp, b.n, "sweep vector")))
+        return fail(rc);
+    for (int gi = 0; gi < n_groups; ++gi) {
+        const GroupDesc &G = a.grp[gi];
+        const int64_t c = (int64_t)G.lens[0] * G.lens[1] * G.lens[2];
+        cudaError_t e = cudaMemcpy(dhats + G.hat_off, hats[gi], c * sizeof(double), cudaMemcpyDefault);
+        if (e != cudaSuccess) return fail(cuda_fail(e, "hat upload", __FILE__, __LINE__));
+    }
+    cudaError_t e = cudaMemcpy(dblocks, blocks, nblk * sizeof(double), cudaMemcpyDefault);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "block upload", __FILE__, __LINE__));
+    a.hats = dhats;
+    a.blocks = dblocks;
+    a.g = geom_of(b);
+    const unsigned long long init[2] = {0ull, ~0ull};
+    e = cudaMemcpy(cnt, init, sizeof init, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "counter init", __FILE__, __LINE__));
+    const int wd = d > 1 ? b.W : 1;
+    const unsigned slot_lines = (unsigned)(d > 2 ? wd * wd : wd);
+    box_raw_kernel<<<dim3((unsigned)a.g.nlines, slot_lines), 128>>>(a, b.values);
+    box_sym_kernel<<<148 * 8, 256>>>(a.g, b.values);
+    box_mask_kernel<<<148 * 8, 256>>>(a.g, b.values, b.mask, cnt, cnt + 1);
+    count_launch(3);
+    unsigned long long host[2];
+    e = cudaMemcpy(host, cnt, sizeof host, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "assembly", __FILE__, __LINE__));
+    LP_CUDA(cudaMemset(m->flags, 0, b.n * sizeof(int)));
+    cudaFree(dhats);
+    cudaFree(dblocks);
+    cudaFree(cnt);
+    b.nnz = (int64_t)host[0];
+    m->nnz = b.nnz;
+    if (b.nnz == 0) {
+        lp_ilu_destroy(m);
+        set_error("assembled preconditioner has no nonzero entries");
+        return LP_ERR_ARG;
+    }
+    // a row without a stored diagonal is reported by lp_ilu0 (IluZeroPivotError(i))
+    m->missing_diag = host[1] != ~0ull ? (int64_t)host[1] : -1;
+    *out = m;
+    return LP_OK;
+}

@@ -1,0 +1,364 @@
+// General-pattern CSR matrices: ILU(0) factorisation, sweeps and SpMV.
+//
+// Reference: sparse.py:116-221.  Used for SparseMatrix objects that do not
+// come from assemble_M (from_dense / from_scipy / Matrix Market).  Matrices
+// assembled by assemble_M use the implicit-offset box kernels (ilu_box.cu).
+//
+// All three triangular kernels are "sync-free": one warp per row, rows handed
+// out in increasing (decreasing for the backward sweep) order through an
+// atomic ticket, and per-row completion flags published with release fences.
+// A warp only ever waits on rows handed out before its own, which are held
+// by resident warps, so the schedule cannot deadlock.  The factorisation
+// keeps the reference's per-row k-ascending order and separately rounded
+// multiply/subtract, so its factors are bit-identical to sparse.py:116-139.
+#include <stdlib.h>
+
+#include <vector>
+
+#include "ilu.cuh"
+
+namespace lp {
+namespace {
+
+constexpr int WARPS_PER_BLOCK = 8;
+
+__device__ __forceinline__ int next_ticket(int *ticket) {
+    int t = 0;
+    if ((threadIdx.x & 31) == 0) t = atomicAdd(ticket, 1);
+    return __shfl_sync(0xffffffff, t, 0);
+}
+
+__device__ __forceinline__ void wait_flag(const int *flags, int64_t k, int epoch) {
+    const volatile int *f = flags + k;
+    while (*f != epoch) {
+    }
+    __threadfence();
+}
+
+__device__ __forceinline__ void publish(int *flags, int64_t row, int epoch) {
+    __threadfence();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+        __threadfence();
+        *((volatile int *)(flags + row)) = epoch;
+    }
+}
+
+__device__ __forceinline__ int64_t find_col(const int32_t *__restrict__ idx, int64_t lo,
+                                            int64_t hi, int32_t col) {
+    int64_t a = lo, b = hi;
+    while (a < b) {
+        const int64_t mid = (a + b) >> 1;
+        if (__ldg(idx + mid) < col) a = mid + 1;
+        else b = mid;
+    }
+    return (a < hi && __ldg(idx + a) == col) ? a : -1;
+}
+
+__global__ void diag_kernel(int64_t n, const int64_t *__restrict__ indptr,
+                            const int32_t *__restrict__ idx, int64_t *__restrict__ diag,
+                            unsigned long long *__restrict__ missing) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t lo = indptr[i], hi = indptr[i + 1];
+    int64_t a = lo, b = hi;
+    while (a < b) {
+        const int64_t m = (a + b) >> 1;
+        if (idx[m] < i) a = m + 1;
+        else b = m;
+    }
+    if (a < hi && idx[a] == i) diag[i] = a;
+    else {
+        diag[i] = -1;
+        atomicMin(missing, (unsigned long long)i);
+    }
+}
+
+__global__ void ilu0_csr_kernel(int64_t n, const int64_t *__restrict__ indptr,
+                                const int32_t *__restrict__ idx, const int64_t *__restrict__ diag,
+                                double *lu, int *flags, int epoch, int *ticket, double tol,
+                                unsigned long long *bad) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        const int64_t row = next_ticket(ticket);
+        if (row >= n) return;
+        const int64_t lo = indptr[row], hi = indptr[row + 1], dr = diag[row];
+        for (int64_t e = lo; e < dr; ++e) {
+            const int64_t k = __ldg(idx + e);
+            if (lane == 0) wait_flag(flags, k, epoch);
+            __syncwarp();
+            const int64_t dk = __ldg(diag + k);
+            const double piv = __ldcg(lu + dk);
+            if (fabs(piv) < tol && lane == 0)
+                atomicMin(bad, (unsigned long long)(row * n + k));
+            const double lik = __ddiv_rn(__ldcg(lu + e), piv);
+            __syncwarp();
+            if (lane == 0) __stcg(lu + e, lik);
+            const int64_t kend = indptr[k + 1];
+            for (int64_t f = dk + 1 + lane; f < kend; f += 32) {
+                const int64_t pos = find_col(idx, lo, hi, __ldg(idx + f));
+                if (pos >= 0) {
+                    const double u = __ldcg(lu + f);
+                    __stcg(lu + pos, __dsub_rn(__ldcg(lu + pos), __dmul_rn(lik, u)));
+                }
+            }
+            __threadfence_block();
+            __syncwarp();
+        }
+        publish(flags, row, epoch);
+    }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+    return v;
+}
+
+__global__ void fwd_csr_kernel(int64_t n, const int64_t *__restrict__ indptr,
+                               const int32_t *__restrict__ idx, const int64_t *__restrict__ diag,
+                               const double *__restrict__ lu, const double *__restrict__ r,
+                               double *y, int *flags, int epoch, int *ticket) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        const int64_t row = next_ticket(ticket);
+        if (row >= n) return;
+        const int64_t lo = indptr[row], dr = diag[row];
+        double acc = 0.0;
+        for (int64_t e = lo + lane; e < dr; e += 32) {
+            const int64_t k = __ldg(idx + e);
+            wait_flag(flags, k, epoch);
+            acc = fma(__ldg(lu + e), __ldcg(y + k), acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) __stcg(y + row, r[row] - acc);
+        publish(flags, row, epoch);
+    }
+}
+
+__global__ void bwd_csr_kernel(int64_t n, const int64_t *__restrict__ indptr,
+                               const int32_t *__restrict__ idx, const int64_t *__restrict__ diag,
+                               const double *__restrict__ lu, const double *__restrict__ y,
+                               double *z, int *flags, int epoch, int *ticket) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        const int64_t t = next_ticket(ticket);
+        if (t >= n) return;
+        const int64_t row = n - 1 - t;
+        const int64_t hi = indptr[row + 1], dr = diag[row];
+        double acc = 0.0;
+        for (int64_t e = dr + 1 + lane; e < hi; e += 32) {
+            const int64_t k = __ldg(idx + e);
+            wait_flag(flags, k, epoch);
+            acc = fma(__ldg(lu + e), __ldcg(z + k), acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) __stcg(z + row, (y[row] - acc) / __ldg(lu + dr));
+        publish(flags, row, epoch);
+    }
+}
+
+__global__ void spmv_csr_kernel(int64_t n, const int64_t *__restrict__ indptr,
+                                const int32_t *__restrict__ idx, const double *__restrict__ v,
+                                const double *__restrict__ x, double *__restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (row >= n) return;
+    double acc = 0.0;
+    for (int64_t e = indptr[row] + lane; e < indptr[row + 1]; e += 32)
+        acc = fma(v[e], x[idx[e]], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) y[row] = acc;
+}
+
+unsigned syncfree_blocks(int64_t n) {
+    int64_t b = ceil_div(n, WARPS_PER_BLOCK);
+    const int64_t cap = 148 * 8;
+    return (unsigned)(b < cap ? b : cap);
+}
+
+int csr_fwd(lp_ilu *m, const double *r, double *y, cudaStream_t st) {
+    const int ep = ++m->epoch;
+    LP_CUDA(cudaMemsetAsync(m->ticket, 0, sizeof(int), st));
+    fwd_csr_kernel<<<syncfree_blocks(m->n), 32 * WARPS_PER_BLOCK, 0, st>>>(
+        m->n, m->indptr, m->indices, m->diag, m->lu, r, y, m->flags, ep, m->ticket);
+    count_launch();
+    LP_CHECK_LAUNCH();
+    return LP_OK;
+}
+
+int csr_bwd(lp_ilu *m, const double *y, double *z, cudaStream_t st) {
+    const int ep = ++m->epoch;
+    LP_CUDA(cudaMemsetAsync(m->ticket, 0, sizeof(int), st));
+    bwd_csr_kernel<<<syncfree_blocks(m->n), 32 * WARPS_PER_BLOCK, 0, st>>>(
+        m->n, m->indptr, m->indices, m->diag, m->lu, y, z, m->flags, ep, m->ticket);
+    count_launch();
+    LP_CHECK_LAUNCH();
+    return LP_OK;
+}
+
+}  // namespace
+
+int ilu_apply(lp_ilu *m, const double *r, double *z, cudaStream_t st) {
+    int rc;
+    if (m->kind == MAT_BOX) {
+        if ((rc = box_forward(m, r, m->ytmp, st))) return rc;
+        return box_backward(m, m->ytmp, z, st);
+    }
+    if ((rc = csr_fwd(m, r, m->ytmp, st))) return rc;
+    return csr_bwd(m, m->ytmp, z, st);
+}
+
+}  // namespace lp
+
+using namespace lp;
+
+static int alloc_sweep_state(lp_ilu *m) {
+    int rc;
+    if ((rc = dalloc(&m->flags, m->n, "row flags")) || (rc = dalloc(&m->ticket, 4, "tickets")) ||
+        (rc = dalloc(&m->bad, 1, "pivot key")) || (rc = dalloc(&m->ytmp, m->n, "sweep vector")))
+        return rc;
+    LP_CUDA(cudaMemset(m->flags, 0, m->n * sizeof(int)));
+    return LP_OK;
+}
+
+extern "C" int lp_csr_create(int64_t n, int64_t nnz, const int64_t *indptr,
+                             const int32_t *indices, const double *values, lp_ilu **out) {
+    *out = nullptr;
+    LP_ARG(n > 0, "empty matrix");
+    LP_ARG(nnz >= 0, "negative nnz");
+    lp_ilu *m = new lp_ilu();
+    m->kind = MAT_CSR;
+    m->n = n;
+    m->nnz = nnz;
+    int rc;
+    if ((rc = dalloc(&m->indptr, n + 1, "indptr")) || (rc = dalloc(&m->indices, nnz, "indices")) ||
+        (rc = dalloc(&m->values, nnz, "values")) || (rc = dalloc(&m->lu, nnz, "factors")) ||
+        (rc = dalloc(&m->diag, n, "diag")) || (rc = alloc_sweep_state(m))) {
+        lp_ilu_destroy(m);
+        return rc;
+    }
+    cudaError_t e = cudaMemcpy(m->indptr, indptr, (n + 1) * sizeof(int64_t), cudaMemcpyDefault);
+    if (e == cudaSuccess && nnz)
+        e = cudaMemcpy(m->indices, indices, nnz * sizeof(int32_t), cudaMemcpyDefault);
+    if (e == cudaSuccess && nnz)
+        e = cudaMemcpy(m->values, values, nnz * sizeof(double), cudaMemcpyDefault);
+    if (e != cudaSuccess) {
+        lp_ilu_destroy(m);
+        return cuda_fail(e, "csr upload", __FILE__, __LINE__);
+    }
+    *out = m;
+    return LP_OK;
+}
+
+extern "C" int lp_ilu_destroy(lp_ilu *m) {
+    if (!m) return LP_OK;
+    void *ptrs[] = {m->indptr, m->indices, m->values, m->lu, m->diag, m->flags, m->ticket,
+                    m->bad, m->ytmp, m->box.values, m->box.lu, m->box.mask};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    delete m;
+    return LP_OK;
+}
+
+extern "C" int lp_matrix_nnz(const lp_ilu *m, int64_t *nnz) {
+    *nnz = m->kind == MAT_BOX ? m->box.nnz : m->nnz;
+    return LP_OK;
+}
+
+extern "C" int lp_ilu0(lp_ilu *m, double tol, int64_t *bad_row, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    *bad_row = -1;
+    if (m->kind == MAT_BOX) return box_ilu0(m, tol, bad_row, st);
+    const int64_t n = m->n;
+    unsigned long long *key = reinterpret_cast<unsigned long long *>(m->bad);
+    const unsigned long long none = ~0ull;
+    LP_CUDA(cudaMemcpyAsync(key, &none, sizeof none, cudaMemcpyHostToDevice, st));
+    diag_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, m->indptr, m->indices, m->diag, key);
+    count_launch();
+    unsigned long long hk;
+    LP_CUDA(cudaMemcpyAsync(&hk, key, sizeof hk, cudaMemcpyDeviceToHost, st));
+    LP_CUDA(cudaStreamSynchronize(st));
+    if (hk != none) {
+        *bad_row = (int64_t)hk;
+        set_error("zero pivot at elimination step %lld", (long long)hk);
+        return LP_ERR_ZERO_PIVOT;
+    }
+    LP_CUDA(cudaMemcpyAsync(m->lu, m->values, m->nnz * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    const int ep = ++m->epoch;
+    LP_CUDA(cudaMemsetAsync(m->ticket, 0, sizeof(int), st));
+    ilu0_csr_kernel<<<syncfree_blocks(n), 32 * WARPS_PER_BLOCK, 0, st>>>(
+        n, m->indptr, m->indices, m->diag, m->lu, m->flags, ep, m->ticket, tol, key);
+    count_launch();
+    LP_CHECK_LAUNCH();
+    int64_t dlast;
+    double plast;
+    LP_CUDA(cudaMemcpyAsync(&hk, key, sizeof hk, cudaMemcpyDeviceToHost, st));
+    LP_CUDA(cudaMemcpyAsync(&dlast, m->diag + (n - 1), sizeof dlast, cudaMemcpyDeviceToHost, st));
+    LP_CUDA(cudaStreamSynchronize(st));
+    LP_CUDA(cudaMemcpy(&plast, m->lu + dlast, sizeof plast, cudaMemcpyDeviceToHost));
+    if (hk != none) *bad_row = (int64_t)(hk % (unsigned long long)n);
+    else if (fabs(plast) < tol) *bad_row = n - 1;
+    if (*bad_row >= 0) {
+        set_error("zero pivot at elimination step %lld", (long long)*bad_row);
+        return LP_ERR_ZERO_PIVOT;
+    }
+    m->factored = true;
+    return LP_OK;
+}
+
+extern "C" int lp_forward_sub(lp_ilu *m, const double *r, double *y, void *stream) {
+    LP_ARG(m->factored, "matrix has not been factored (call lp_ilu0)");
+    if (m->kind == MAT_BOX) return box_forward(m, r, y, as_stream(stream));
+    return csr_fwd(m, r, y, as_stream(stream));
+}
+
+extern "C" int lp_backward_sub(lp_ilu *m, const double *y, double *z, void *stream) {
+    LP_ARG(m->factored, "matrix has not been factored (call lp_ilu0)");
+    if (m->kind == MAT_BOX) return box_backward(m, y, z, as_stream(stream));
+    return csr_bwd(m, y, z, as_stream(stream));
+}
+
+extern "C" int lp_precond_apply(lp_ilu *m, const double *r, double *z, void *stream) {
+    LP_ARG(m->factored, "matrix has not been factored (call lp_ilu0)");
+    return ilu_apply(m, r, z, as_stream(stream));
+}
+
+extern "C" int lp_spmv(lp_ilu *m, const double *x, double *y, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    if (m->kind == MAT_BOX) return box_spmv(m, x, y, st);
+    spmv_csr_kernel<<<(unsigned)ceil_div(m->n * 32, 256), 256, 0, st>>>(m->n, m->indptr,
+                                                                       m->indices, m->values, x, y);
+    count_launch();
+    LP_CHECK_LAUNCH();
+    return LP_OK;
+}
+
+extern "C" int lp_matrix_export(const lp_ilu *m, int which, int64_t *indptr, int32_t *indices,
+                                double *values) {
+    LP_ARG(which >= 0 && which <= 2, "which must be 0 (M), 1 (L) or 2 (U)");
+    LP_ARG(which == 0 || m->factored, "matrix has not been factored");
+    if (m->kind == MAT_BOX) return box_export(m, which, indptr, indices, values);
+    const int64_t n = m->n, nnz = m->nnz;
+    std::vector<int64_t> ip(n + 1), dg(n);
+    std::vector<int32_t> ix(nnz);
+    std::vector<double> v(nnz);
+    LP_CUDA(cudaMemcpy(ip.data(), m->indptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    LP_CUDA(cudaMemcpy(ix.data(), m->indices, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    LP_CUDA(cudaMemcpy(v.data(), which == 0 ? m->values : m->lu, nnz * sizeof(double),
+                       cudaMemcpyDeviceToHost));
+    if (which) LP_CUDA(cudaMemcpy(dg.data(), m->diag, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    int64_t out = 0;
+    indptr[0] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t a = ip[i], b = ip[i + 1];
+        if (which == 1) b = dg[i];
+        if (which == 2) a = dg[i];
+        for (int64_t e = a; e < b; ++e, ++out) {
+            if (indices) indices[out] = ix[e];
+            if (values) values[out] = v[e];
+        }
+        indptr[i + 1] = out;
+    }
+    return LP_OK;
+}

@@ -1,0 +1,57 @@
+"""Device-buffer plumbing (torch owns device memory and streams)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+
+def torch():
+    import torch as _t
+    return _t
+
+
+def is_device(a):
+    t = torch()
+    return isinstance(a, t.Tensor) and a.is_cuda
+
+
+def to_device(a):
+    """float64 contiguous CUDA tensor holding `a` (numpy/torch) in memory order."""
+    t = torch()
+    _lib.load()
+    if isinstance(a, t.Tensor):
+        return a.to(device="cuda", dtype=t.float64).contiguous()
+    arr = np.ascontiguousarray(a, dtype=np.float64)
+    return t.from_numpy(arr).to("cuda", non_blocking=False)
+
+
+def empty(n):
+    t = torch()
+    _lib.load()
+    return t.empty(int(n), dtype=t.float64, device="cuda")
+
+
+def ptr(tensor):
+    return tensor.data_ptr() if tensor is not None else None
+
+
+def host(tensor):
+    return tensor.detach().cpu().numpy()
+
+
+def fortran_flat(data):
+    """K^d tensor (axis 0 = x) -> x-fastest flat layout (pcg.py:135)."""
+    if is_device(data):
+        d = data.dim()
+        return data.permute(*reversed(range(d))).contiguous().reshape(-1)
+    return np.asarray(data, dtype=float).flatten(order="F")
+
+
+def from_fortran_flat(flat, K, d):
+    """x-fastest flat vector -> K^d C-order ndarray / tensor with axis 0 = x."""
+    if is_device(flat):
+        v = flat.reshape((K,) * d)
+        return v.permute(*reversed(range(d))).contiguous()
+    return np.ascontiguousarray(np.asarray(flat).reshape((K,) * d, order="F"))

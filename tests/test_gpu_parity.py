@@ -1,0 +1,275 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden vectors and the CPU oracle on identical seeded inputs."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import legpcg_port as orc  # noqa: E402
+from paper_2004_13961_b200 import (ProblemSpec, SolverConfig, SpectralCoeffs,  # noqa: E402
+                                   TransformPlan, apply_A, apply_B, apply_system,
+                                   assemble_M, backward_sub, forward_sub, ilu0,
+                                   pcg_solve, precond_apply, tensor_bdlt, tensor_fdlt,
+                                   workloads as wl)
+from paper_2004_13961_b200.coefficients import CoefficientField  # noqa: E402
+from paper_2004_13961_b200.sparse import SparseMatrix  # noqa: E402
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def relerr(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    den = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (den if den > 0 else 1.0)
+
+
+def probe(v, seed=99):
+    v = np.asarray(v, dtype=float).ravel()
+    g = np.random.default_rng(seed).standard_normal(v.size)
+    return np.array([v.sum(), np.abs(v).sum(), float(v @ g), float(v @ v)])
+
+
+def spec_of(w, N):
+    return ProblemSpec(dim=w.dim, N=N, beta=w.beta, alpha=w.alpha, rhs=w.rhs_field)
+
+
+# ------------------------------------------------------------------ transforms
+
+@pytest.mark.parametrize("P", [129, 257, 513, 2049])
+def test_device_table_bitwise(golden, P):
+    assert sha(TransformPlan(P).table()) == str(golden("quadrature")[f"table{P}_sha"])
+
+
+@pytest.mark.parametrize("d,P", [(1, 33), (2, 17), (3, 9), (2, 129)])
+def test_tensor_transforms(golden, d, P):
+    g = golden("transforms")
+    plan = TransformPlan(P)
+    k = f"tr{d}d{P}"
+    assert relerr(tensor_bdlt(plan, g[k + "_c"]), g[k + "_bdlt"]) < 1e-13
+    assert relerr(tensor_fdlt(plan, g[k + "_f"]), g[k + "_fdlt"]) < 1e-13
+
+
+def test_transform_known_answers():
+    # reference tests/test_transforms.py:22-31,49-59
+    plan = TransformPlan(33)
+    e0 = np.zeros(33)
+    e0[0] = 1.0
+    np.testing.assert_allclose(tensor_bdlt(plan, e0), np.ones(33), atol=1e-14)
+    np.testing.assert_allclose(tensor_fdlt(plan, np.ones(33)), e0, atol=1e-13)
+    e1 = np.zeros(33)
+    e1[1] = 1.0
+    np.testing.assert_allclose(tensor_fdlt(plan, plan.rule.nodes.copy()), e1, atol=1e-13)
+
+
+# ---------------------------------------------------------------------- matvec
+
+MV = [("cfg1", 16), ("cfg1", 128), ("cfg2", 24), ("cfg2", 256), ("cfg3", 64), ("cfg4", 10),
+      ("cfg4", 24), ("cfg5", 12)]
+
+
+@pytest.mark.parametrize("name,N", MV)
+def test_matvec_golden(golden, name, N):
+    g = golden("matvec")
+    w = wl.CONFIGS[name]()
+    spec = spec_of(w, N)
+    plan = TransformPlan(N + 1)
+    u = SpectralCoeffs(np.random.default_rng(7).standard_normal((N - 1,) * w.dim))
+    k = f"mv_{name}_N{N}"
+    assert relerr(apply_A(spec, plan, u).data, g[k + "_A"]) < 1e-12
+    assert relerr(apply_B(spec, plan, u).data, g[k + "_B"]) < 1e-12
+    assert relerr(apply_system(spec, plan, u).data, g[k + "_sys"]) < 1e-12
+
+
+def test_matvec_axis_betas(golden):
+    ab = (CoefficientField(1, lambda x: np.exp(2 * x), "e2x"),
+          CoefficientField(1, np.cos, "cosx"), CoefficientField(1, np.cos, "cosx"))
+    spec = ProblemSpec(dim=3, N=8, axis_betas=ab,
+                       alpha=CoefficientField(3, lambda x, y, z: 1 + x * x, "1+x2"))
+    u = SpectralCoeffs(np.random.default_rng(8).standard_normal((7, 7, 7)))
+    out = apply_system(spec, TransformPlan(9), u).data
+    assert relerr(out, golden("matvec")["mv_axisbeta3d_N8_sys"]) < 1e-12
+
+
+@pytest.mark.parametrize("name,N", [("cfg3", 2048), ("cfg4", 128)])
+def test_matvec_full_size_vs_oracle(name, N):
+    """BASELINE sizes: <= 1e-12 relative against the CPU oracle."""
+    w = wl.CONFIGS[name]()
+    spec = spec_of(w, N)
+    u = np.random.default_rng(3).standard_normal((N - 1,) * w.dim)
+    ref = orc.apply_system(spec, orc.Plan(N + 1), u)
+    out = apply_system(spec, TransformPlan(N + 1), SpectralCoeffs(u)).data
+    assert relerr(out, ref) < 1e-12
+
+
+def test_matvec_constant_coefficient_known_answers():
+    # reference tests/test_operator.py:26-34 (A e_k = (4k+6) e_k) and :84-95
+    n = 10
+    spec = ProblemSpec(dim=1, N=n, beta=wl.constant_field(1, 1.0),
+                       alpha=wl.constant_field(1, 1.0))
+    plan = TransformPlan(n + 1)
+    ks = np.arange(n - 1)
+    mass = np.diag(2 / (2 * ks + 1) + 2 / (2 * ks + 5))
+    off = -2 / (2 * ks[:-2] + 5)
+    mass += np.diag(off, 2) + np.diag(off, -2)
+    for k in range(n - 1):
+        e = np.zeros(n - 1)
+        e[k] = 1.0
+        a = apply_A(spec, plan, SpectralCoeffs(e)).data
+        expect = np.zeros(n - 1)
+        expect[k] = 4 * k + 6
+        np.testing.assert_allclose(a, expect, atol=1e-11)
+        np.testing.assert_allclose(apply_B(spec, plan, SpectralCoeffs(e)).data, mass[:, k],
+                                   atol=1e-12)
+
+
+def test_nonpositive_diffusion_rejected():
+    spec = ProblemSpec(dim=1, N=8, beta=CoefficientField(1, lambda x: x, "x"))
+    with pytest.raises(ValueError, match="not positive"):
+        apply_A(spec, TransformPlan(9), SpectralCoeffs(np.ones(7)))
+
+
+def test_device_resident_matvec_matches_host():
+    w = wl.cfg4(N=24)
+    spec = spec_of(w, 24)
+    plan = TransformPlan(25)
+    u = np.random.default_rng(4).standard_normal((23,) * 3)
+    host = apply_system(spec, plan, SpectralCoeffs(u)).data
+    dev = apply_system(spec, plan, SpectralCoeffs(torch.from_numpy(u).cuda())).data
+    np.testing.assert_array_equal(dev.cpu().numpy(), host)
+
+
+# --------------------------------------------------------------- preconditioner
+
+PRE = [("cfg1", 32, 8), ("cfg2", 16, 4), ("cfg2", 20, 10), ("cfg3", 20, 12), ("cfg4", 10, 2),
+       ("cfg4", 12, 8), ("cfg5", 12, 3)]
+
+
+@pytest.mark.parametrize("name,N,T", PRE)
+def test_assemble_M(golden, name, N, T):
+    g = golden("precond")
+    w = wl.CONFIGS[name]()
+    k = f"pc_{name}_N{N}_T{T}"
+    m = assemble_M(spec_of(w, N), T, T)
+    assert m.nnz == int(g[k + "_nnz"])
+    assert sha(m.indptr, m.indices.astype(np.int64)) == str(g[k + "_pattern_sha"])
+    np.testing.assert_allclose(probe(m.values), g[k + "_values_probe"], rtol=1e-12)
+    if k + "_values" in g:
+        assert relerr(m.values, g[k + "_values"]) < 1e-14
+
+
+@pytest.mark.parametrize("name,N,T", PRE)
+def test_ilu0_and_sweeps_box(golden, name, N, T):
+    """Factor the GPU-assembled M in the box layout; compare with the
+    reference's factors and sweeps (tolerance: M itself differs by ~1e-16)."""
+    g = golden("precond")
+    w = wl.CONFIGS[name]()
+    k = f"pc_{name}_N{N}_T{T}"
+    f = ilu0(assemble_M(spec_of(w, N), T, T))
+    np.testing.assert_allclose(probe(f.L.values), g[k + "_L_probe"], rtol=1e-9)
+    np.testing.assert_allclose(probe(f.U.values), g[k + "_U_probe"], rtol=1e-9)
+    assert relerr(forward_sub(f, g[k + "_r"]), g[k + "_fwd"]) < 1e-11
+    assert relerr(precond_apply(f, g[k + "_r"]), g[k + "_z"]) < 1e-11
+
+
+@pytest.mark.parametrize("name,N,T", [c for c in PRE if c != ("cfg4", 12, 8)])
+def test_ilu0_csr_bitwise(golden, name, N, T):
+    """The general CSR kernel on the reference's own M reproduces its
+    factors bit for bit (same k order, separately rounded mul/sub)."""
+    g = golden("precond")
+    k = f"pc_{name}_N{N}_T{T}"
+    if k + "_values" not in g:
+        pytest.skip("M too large for a committed fixture")
+    n = g[k + "_indptr"].size - 1
+    m = SparseMatrix(n, g[k + "_indptr"], g[k + "_indices"], g[k + "_values"])
+    f = ilu0(m)
+    assert sha(f.L.values) == str(g[k + "_L_sha"])
+    assert sha(f.U.values) == str(g[k + "_U_sha"])
+    assert relerr(precond_apply(f, g[k + "_r"]), g[k + "_z"]) < 1e-13
+
+
+def test_sparse_known_answers():
+    # reference tests/test_sparse.py:144-160
+    d = np.array([[1.0, 0, 0], [0.5, 1.0, 0], [0, 0.5, 1.0]])
+    f = ilu0(SparseMatrix.from_dense(d))
+    np.testing.assert_allclose(forward_sub(f, np.ones(3)), [1.0, 0.5, 0.75], atol=1e-15)
+    d = np.array([[2.0, 1.0], [0.0, 4.0]])
+    f = ilu0(SparseMatrix.from_dense(d))
+    np.testing.assert_allclose(backward_sub(f, np.array([3.0, 8.0])), [0.5, 2.0], atol=1e-15)
+    f = ilu0(SparseMatrix.from_dense(np.diag([2.0, 5.0])))
+    np.testing.assert_allclose(precond_apply(f, np.array([4.0, 10.0])), [2.0, 2.0])
+
+
+def test_zero_pivot_and_missing_diagonal():
+    from paper_2004_13961_b200 import IluZeroPivotError
+    with pytest.raises(IluZeroPivotError) as err:
+        ilu0(SparseMatrix.from_dense(np.array([[1.0, 1.0], [1.0, 1.0]])))
+    assert err.value.row == 1
+    with pytest.raises(IluZeroPivotError) as err:
+        ilu0(SparseMatrix.from_dense(np.array([[0.0, 1.0], [1.0, 0.0]])))
+    assert err.value.row == 0
+
+
+def test_full_pattern_is_exact_solve():
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((12, 12))
+    a = a @ a.T + 12 * np.eye(12)
+    f = ilu0(SparseMatrix.from_dense(a))
+    r = rng.standard_normal(12)
+    np.testing.assert_allclose(precond_apply(f, r), np.linalg.solve(a, r), atol=1e-10)
+
+
+# ------------------------------------------------------------------------ PCG
+
+PCG = [("cfg1", 128, 8), ("cfg2", 32, 10), ("cfg2", 256, 10), ("cfg3", 64, 12), ("cfg4", 12, 8),
+       ("cfg5", 16, 8)]
+
+
+@pytest.mark.parametrize("name,N,T", PCG)
+def test_pcg_golden(golden, name, N, T):
+    g = golden("pcg")
+    w = wl.CONFIGS[name]()
+    k = f"pcg_{name}_N{N}_T{T}"
+    spec = spec_of(w, N)
+    x, rep = pcg_solve(spec, SolverConfig(epsilon=w.rtol, preconditioner=(T, T)),
+                       TransformPlan(N + 1), SpectralCoeffs(g[k + "_F"]))
+    assert rep.converged
+    assert abs(rep.iterations - int(g[k + "_iters"])) <= 1
+    assert relerr(x.data, g[k + "_x"]) < 1e-10
+    assert rep.residual_history.size == rep.iterations + 1
+
+
+def test_pcg_determinism():
+    w = wl.cfg2(N=32)
+    spec = spec_of(w, 32)
+    plan = TransformPlan(33)
+    F = SpectralCoeffs(wl.mass_contract_series(w.fhat))
+    cfg = SolverConfig(epsilon=1e-10, preconditioner=(10, 10))
+    x1, r1 = pcg_solve(spec, cfg, plan, F)
+    x2, r2 = pcg_solve(spec, cfg, plan, F)
+    assert r1.iterations == r2.iterations
+    np.testing.assert_array_equal(x1.data, x2.data)
+
+
+def test_pcg_indefinite_and_kmax():
+    from paper_2004_13961_b200 import IndefiniteOperatorError
+    spec = ProblemSpec(dim=1, N=16, beta=wl.constant_field(1, 0.01),
+                       alpha=wl.constant_field(1, -100.0))
+    with pytest.raises(IndefiniteOperatorError) as err:
+        pcg_solve(spec, SolverConfig(epsilon=1e-10), TransformPlan(17),
+                  SpectralCoeffs(np.ones(15)))
+    assert err.value.iteration >= 1
+    w = wl.cfg2(N=16)
+    spec = spec_of(w, 16)
+    _, rep = pcg_solve(spec, SolverConfig(epsilon=1e-14, k_max=2), TransformPlan(17),
+                       SpectralCoeffs(np.ones((15, 15))))
+    assert not rep.converged and rep.iterations == 2
