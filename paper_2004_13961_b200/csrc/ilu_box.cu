@@ -253,7 +253,7 @@ box_ilu0_kernel(Geom g, double *lu, const uint32_t *__restrict__ mask, int *flag
                 for (int q = tyz; q < ny * nz; q += nyz_threads) {
                     const int syp = g.d > 1 ? ylo + q % ny : g.r;
                     const int szp = g.d > 2 ? zlo + q / ny : g.r;
-                    const int sp = sxp + g.W * (syp + g.W * szp);
+                    const int sp = sxp + (g.d > 1 ? g.W * syp : 0) + (g.d > 2 ? g.W * g.W * szp : 0);
                     if (sp <= g.c || !xok) continue;
                     if (g.d > 1) {
                         const int cy = ky + syp - g.r;
@@ -263,7 +263,8 @@ box_ilu0_kernel(Geom g, double *lu, const uint32_t *__restrict__ mask, int *flag
                         const int cz = kz + szp - g.r;
                         if (cz < 0 || cz >= g.K) continue;
                     }
-                    const int t = (sx + sxp - g.r) + g.W * ((sy + syp - g.r) + g.W * (sz + szp - g.r));
+                    const int t = (sx + sxp - g.r) + (g.d > 1 ? g.W * (sy + syp - g.r) : 0) +
+                                  (g.d > 2 ? g.W * g.W * (sz + szp - g.r) : 0);
                     if (!((bits[t >> 5] >> (t & 31)) & 1u)) continue;
                     row[t] = __dsub_rn(row[t], __dmul_rn(l, __ldcg(uk + sp)));
                 }
