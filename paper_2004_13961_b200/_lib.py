@@ -12,7 +12,8 @@ import ctypes
 import os
 import threading
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "liblegpcg_b200.so")
+LIB_PATH = os.environ.get("LP_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "liblegpcg_b200.so")
 
 LP_OK = 0
 LP_ERR_CUDA = -1

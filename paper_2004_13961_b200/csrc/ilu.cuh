@@ -21,6 +21,9 @@ struct BoxLayout {
     uint32_t *mask = nullptr;         // in-pattern bits        [n][ceil(S/32)] (null: all valid slots)
     int mask_words = 0;
     int64_t nnz = 0;
+    // compact in-line bands of the factors for the sweeps' serial recurrence:
+    // band_lo[row][q] = L(row, row-1-q), band_up[row][q] = U(row, row+1+q), q < r
+    double *band_lo = nullptr, *band_up = nullptr, *diag = nullptr;
 };
 
 }  // namespace lp
@@ -53,4 +56,6 @@ int box_backward(lp_ilu *m, const double *y, double *z, cudaStream_t st);
 int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st);
 int box_spmv(lp_ilu *m, const double *x, double *y, cudaStream_t st);
 int box_export(const lp_ilu *m, int which, int64_t *indptr, int32_t *indices, double *values);
+int box_build_bands(lp_ilu *m, cudaStream_t st);
+int box_apply(lp_ilu *m, const double *r, double *z, cudaStream_t st);
 }  // namespace lp

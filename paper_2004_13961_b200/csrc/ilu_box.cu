@@ -16,56 +16,11 @@
 
 #include <vector>
 
+#include "box_geom.cuh"
 #include "ilu.cuh"
 
 namespace lp {
 namespace {
-
-struct Geom {
-    int d, K, r, W, S, c, mw;   // mw = mask words per row
-    int64_t n;
-    int nlines;
-};
-
-Geom geom_of(const BoxLayout &b) {
-    Geom g;
-    g.d = b.d;
-    g.K = b.K;
-    g.r = b.r;
-    g.W = b.W;
-    g.S = b.S;
-    g.c = (b.S - 1) / 2;
-    g.mw = b.mask_words;
-    g.n = b.n;
-    g.nlines = (int)(b.n / b.K);
-    return g;
-}
-
-__device__ __forceinline__ void slot_axes(const Geom &g, int s, int &sx, int &sy, int &sz) {
-    sx = s % g.W;
-    const int q = s / g.W;
-    sy = g.d > 1 ? q % g.W : g.r;
-    sz = g.d > 2 ? q / g.W : g.r;
-}
-
-__device__ __forceinline__ void row_pos(const Geom &g, int64_t i, int &ix, int &iy, int &iz) {
-    ix = (int)(i % g.K);
-    const int64_t q = i / g.K;
-    iy = g.d > 1 ? (int)(q % g.K) : 0;
-    iz = g.d > 2 ? (int)(q / g.K) : 0;
-}
-
-// Column of slot s for row i, or -1 if it leaves the grid.
-__device__ __forceinline__ int64_t slot_col(const Geom &g, int64_t i, int ix, int iy, int iz,
-                                            int s) {
-    int sx, sy, sz;
-    slot_axes(g, s, sx, sy, sz);
-    const int ox = sx - g.r, oy = sy - g.r, oz = sz - g.r;
-    if (ix + ox < 0 || ix + ox >= g.K) return -1;
-    if (g.d > 1 && (iy + oy < 0 || iy + oy >= g.K)) return -1;
-    if (g.d > 2 && (iz + oz < 0 || iz + oz >= g.K)) return -1;
-    return i + ox + (int64_t)g.K * (oy + (int64_t)g.K * oz);
-}
 
 // ----------------------------------------------------------------- assembly
 
@@ -281,111 +236,10 @@ box_ilu0_kernel(Geom g, double *lu, const uint32_t *__restrict__ mask, int *flag
     }
 }
 
-// ------------------------------------------------------------------- sweeps
-//
-// Warp per x-line, lines handed out in natural (reverse) order by a ticket;
-// rows of a line are swept in order by the warp.  Row (ix, line) needs the
-// rows ix' <= ix + r of every earlier line in its stencil; by induction it
-// suffices to wait on the previous line of the same plane and on line
-// (min(iy + r, K-1), iz - 1) of the previous plane.  Per-line progress
-// counters are 64-bit: epoch * (K + 1) + rows done.
-
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
     return v;
-}
-
-__device__ __forceinline__ void wait_progress(const long long *prog, int line, long long need,
-                                              long long &seen) {
-    if (line < 0 || seen >= need) return;
-    const volatile long long *p = prog + line;
-    long long v;
-    while ((v = *p) < need) {
-    }
-    seen = v;
-    __threadfence();
-}
-
-__global__ void box_fwd_kernel(Geom g, const double *__restrict__ lu, const double *__restrict__ rhs,
-                               double *y, long long *prog, long long base, int *ticket) {
-    const int lane = threadIdx.x & 31;
-    for (;;) {
-        int L = 0;
-        if (lane == 0) L = atomicAdd(ticket, 1);
-        L = __shfl_sync(0xffffffff, L, 0);
-        if (L >= g.nlines) return;
-        const int iy = g.d > 1 ? L % g.K : 0, iz = g.d > 2 ? L / g.K : 0;
-        const int dep1 = (g.d > 1 && iy > 0) ? L - 1 : -1;
-        const int dep2 = (g.d > 2 && iz > 0) ? min(iy + g.r, g.K - 1) + g.K * (iz - 1) : -1;
-        long long seen1 = -1, seen2 = -1;
-        for (int ix = 0; ix < g.K; ++ix) {
-            if (lane == 0) {
-                const long long need = base + min(g.K, ix + g.r + 1);
-                wait_progress(prog, dep1, need, seen1);
-                wait_progress(prog, dep2, need, seen2);
-            }
-            __syncwarp();
-            const int64_t i = (int64_t)L * g.K + ix;
-            const double *lr = lu + (size_t)i * g.S;
-            double acc = 0.0;
-            for (int s = lane; s < g.c; s += 32) {
-                const double v = __ldg(lr + s);
-                if (v != 0.0) {
-                    const int64_t col = slot_col(g, i, ix, iy, iz, s);
-                    acc = fma(v, __ldcg(y + col), acc);
-                }
-            }
-            acc = warp_sum(acc);
-            if (lane == 0) {
-                __stcg(y + i, rhs[i] - acc);
-                __threadfence();
-                *((volatile long long *)(prog + L)) = base + ix + 1;
-            }
-            __syncwarp();
-        }
-    }
-}
-
-__global__ void box_bwd_kernel(Geom g, const double *__restrict__ lu, const double *__restrict__ rhs,
-                               double *z, long long *prog, long long base, int *ticket) {
-    const int lane = threadIdx.x & 31;
-    for (;;) {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(ticket, 1);
-        t = __shfl_sync(0xffffffff, t, 0);
-        if (t >= g.nlines) return;
-        const int L = g.nlines - 1 - t;
-        const int iy = g.d > 1 ? L % g.K : 0, iz = g.d > 2 ? L / g.K : 0;
-        const int dep1 = (g.d > 1 && iy < g.K - 1) ? L + 1 : -1;
-        const int dep2 = (g.d > 2 && iz < g.K - 1) ? max(iy - g.r, 0) + g.K * (iz + 1) : -1;
-        long long seen1 = -1, seen2 = -1;
-        for (int ix = g.K - 1; ix >= 0; --ix) {
-            if (lane == 0) {
-                const long long need = base + min(g.K, g.K - ix + g.r);
-                wait_progress(prog, dep1, need, seen1);
-                wait_progress(prog, dep2, need, seen2);
-            }
-            __syncwarp();
-            const int64_t i = (int64_t)L * g.K + ix;
-            const double *ur = lu + (size_t)i * g.S;
-            double acc = 0.0;
-            for (int s = g.c + 1 + lane; s < g.S; s += 32) {
-                const double v = __ldg(ur + s);
-                if (v != 0.0) {
-                    const int64_t col = slot_col(g, i, ix, iy, iz, s);
-                    acc = fma(v, __ldcg(z + col), acc);
-                }
-            }
-            acc = warp_sum(acc);
-            if (lane == 0) {
-                __stcg(z + i, (rhs[i] - acc) / __ldg(ur + g.c));
-                __threadfence();
-                *((volatile long long *)(prog + L)) = base + (g.K - ix);
-            }
-            __syncwarp();
-        }
-    }
 }
 
 __global__ void box_spmv_kernel(Geom g, const double *__restrict__ vals, const double *__restrict__ x,
@@ -404,41 +258,7 @@ __global__ void box_spmv_kernel(Geom g, const double *__restrict__ vals, const d
     if (lane == 0) y[i] = acc;
 }
 
-constexpr int SWEEP_WARPS = 4;
-
-unsigned sweep_blocks(int nlines) {
-    const int cap = 148 * 16;
-    const int b = (nlines + SWEEP_WARPS - 1) / SWEEP_WARPS;
-    return (unsigned)(b < cap ? b : cap);
-}
-
 }  // namespace
-
-// progress counters live in the generic `flags` buffer of the handle (sized for n ints,
-// which is >= 2 * nlines ints for K >= 2)
-static long long *box_prog(lp_ilu *m) { return reinterpret_cast<long long *>(m->flags); }
-
-int box_forward(lp_ilu *m, const double *r, double *y, cudaStream_t st) {
-    Geom g = geom_of(m->box);
-    const long long base = (long long)(++m->epoch) * (g.K + 1);
-    LP_CUDA(cudaMemsetAsync(m->ticket, 0, sizeof(int), st));
-    box_fwd_kernel<<<sweep_blocks(g.nlines), 32 * SWEEP_WARPS, 0, st>>>(
-        g, m->box.lu, r, y, box_prog(m), base, m->ticket);
-    count_launch();
-    LP_CHECK_LAUNCH();
-    return LP_OK;
-}
-
-int box_backward(lp_ilu *m, const double *y, double *z, cudaStream_t st) {
-    Geom g = geom_of(m->box);
-    const long long base = (long long)(++m->epoch) * (g.K + 1);
-    LP_CUDA(cudaMemsetAsync(m->ticket, 0, sizeof(int), st));
-    box_bwd_kernel<<<sweep_blocks(g.nlines), 32 * SWEEP_WARPS, 0, st>>>(
-        g, m->box.lu, y, z, box_prog(m), base, m->ticket);
-    count_launch();
-    LP_CHECK_LAUNCH();
-    return LP_OK;
-}
 
 int box_spmv(lp_ilu *m, const double *x, double *y, cudaStream_t st) {
     Geom g = geom_of(m->box);
@@ -520,7 +340,7 @@ int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st) {
         return LP_ERR_ZERO_PIVOT;
     }
     m->factored = true;
-    return LP_OK;
+    return box_build_bands(m, st);
 }
 
 int box_export(const lp_ilu *m, int which, int64_t *indptr, int32_t *indices, double *values) {

@@ -201,10 +201,7 @@ int csr_bwd(lp_ilu *m, const double *y, double *z, cudaStream_t st) {
 
 int ilu_apply(lp_ilu *m, const double *r, double *z, cudaStream_t st) {
     int rc;
-    if (m->kind == MAT_BOX) {
-        if ((rc = box_forward(m, r, m->ytmp, st))) return rc;
-        return box_backward(m, m->ytmp, z, st);
-    }
+    if (m->kind == MAT_BOX) return box_apply(m, r, z, st);
     if ((rc = csr_fwd(m, r, m->ytmp, st))) return rc;
     return csr_bwd(m, m->ytmp, z, st);
 }
@@ -254,7 +251,8 @@ extern "C" int lp_csr_create(int64_t n, int64_t nnz, const int64_t *indptr,
 extern "C" int lp_ilu_destroy(lp_ilu *m) {
     if (!m) return LP_OK;
     void *ptrs[] = {m->indptr, m->indices, m->values, m->lu, m->diag, m->flags, m->ticket,
-                    m->bad, m->ytmp, m->box.values, m->box.lu, m->box.mask};
+                    m->bad, m->ytmp, m->box.values, m->box.lu, m->box.mask,
+                    m->box.band_lo, m->box.band_up, m->box.diag};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete m;

@@ -1,0 +1,45 @@
+"""Per-line timeline of the box sweep (dev tool; needs the LP_SWEEP_TRACE build)."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2004_13961_b200 import ProblemSpec, TransformPlan, _lib, workloads as wl  # noqa: E402
+from paper_2004_13961_b200.precond import assemble_M  # noqa: E402
+from paper_2004_13961_b200.sparse import ilu0  # noqa: E402
+
+name = sys.argv[1]
+w = wl.CONFIGS[name]()
+spec = ProblemSpec(dim=w.dim, N=w.N, beta=w.beta, alpha=w.alpha)
+f = ilu0(assemble_M(spec, w.T, w.T, TransformPlan(w.N + 1)))
+lib = _lib.load()
+n = w.dofs
+r = torch.randn(n, dtype=torch.float64, device="cuda")
+y = torch.empty_like(r)
+for _ in range(3):
+    lib.lp_forward_sub(f._handle, r.data_ptr(), y.data_ptr(), _lib.stream_ptr())
+torch.cuda.synchronize()
+nl = n // w.K
+buf = np.zeros(nl * 4, dtype=np.uint64)
+lib.lp_debug_sweep_trace.restype = ctypes.c_int
+lib.lp_debug_sweep_trace(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_int64(buf.size))
+t = buf.reshape(nl, 4).astype(np.int64)
+t0 = t[:, 0].min()
+t = (t - t0) / 1e3
+print(name, "line  start  row0  rowmid  rowlast   (us)")
+for L in list(range(0, 12)) + list(range(nl // 2, nl // 2 + 4)) + list(range(nl - 4, nl)):
+    print(L, *[f"{v:9.2f}" for v in t[L]])
+d0 = np.diff(t[:, 1])
+print("lead (row0 to row0) median us", np.median(d0), "line duration median",
+      np.median(t[:, 3] - t[:, 1]), "start->row0 median", np.median(t[:, 1] - t[:, 0]))
+buf2 = np.zeros(nl * 4 + 12 * w.K, dtype=np.uint64)
+lib.lp_debug_sweep_trace(buf2.ctypes.data_as(ctypes.c_void_p), ctypes.c_int64(buf2.size))
+rows = buf2[nl * 4:].reshape(2, w.K, 6).astype(np.int64)
+for which in (0, 1):
+    rr = (rows[which][:, :5] - t0) / 1e3
+    print("line", nl // 2 - 1 + which, "t: proc_start polled gathered written consumed | npolls")
+    for tt in list(range(0, 20)) + list(range(w.K // 2, w.K // 2 + 24)):
+        print(tt, *[f"{rr[tt][c]:9.2f}" for c in (0, 4, 1, 2, 3)], "|", rows[which][tt][5])
