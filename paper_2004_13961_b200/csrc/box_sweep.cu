@@ -466,9 +466,9 @@ int launch_sweep(lp_ilu *m, const double *rhs, double *out, cudaStream_t st) {
         static unsigned long long *tr = nullptr;
         static size_t trn = 0;
         if (trn < (size_t)g.nlines * 4 + (size_t)12 * g.K) {
-            if (tr) cudaFree(tr);
+            if (tr) dfree(tr);
             trn = (size_t)g.nlines * 4 + (size_t)12 * g.K;
-            cudaMalloc(&tr, trn * 8);
+            dalloc(&tr, trn, "sweep trace");
         }
         cudaMemsetAsync(tr, 0, trn * 8, st);
         a.trace = tr;

@@ -127,6 +127,18 @@ __global__ void box_mask_kernel(Geom g, double *vals, uint32_t *mask,
     if (lane == 0 && cnt) atomicAdd(nnz, cnt);
 }
 
+// full[i] = 1 when every slot of row i is in the pattern (interior rows of a
+// full box): the factorisation then needs no boundary or pattern checks.
+__global__ void box_full_kernel(Geom g, const uint32_t *__restrict__ mask,
+                                unsigned char *__restrict__ full) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int cnt = 0;
+        for (int w = 0; w < g.mw; ++w) cnt += __popc(mask[(size_t)i * g.mw + w]);
+        full[i] = cnt == g.S;
+    }
+}
+
 // ----------------------------------------------------------- factorisation
 //
 // IKJ ILU(0) (sparse.py:116-139) with one CTA per row, rows handed out in
@@ -139,6 +151,12 @@ __global__ void box_mask_kernel(Geom g, double *vals, uint32_t *mask,
 // its updates in the reference's k order, each as a separately rounded
 // multiply and subtract: the factors are bit-identical to the reference's for
 // the same M.
+
+__device__ __forceinline__ int ld_flag(const int *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
 template <int TPR>
 __device__ __forceinline__ void row_sync() {
@@ -175,13 +193,10 @@ box_ilu0_kernel(Geom g, double *lu, const uint32_t *__restrict__ mask, int *flag
             int sx, sy, sz;
             slot_axes(g, s, sx, sy, sz);
             const int64_t k = i + (sx - g.r) + (int64_t)g.K * ((sy - g.r) + (int64_t)g.K * (sz - g.r));
-            if (tid == 0) {
-                const volatile int *f = flags + k;
-                while (*f != epoch) {
-                }
-                __threadfence();
+            // all threads poll the same flag (uniform, no divergent spin); the
+            // writer fences before publishing, and row k is read through L2
+            while (ld_flag(flags + k) != epoch) {
             }
-            row_sync<TPR>();
             const double *uk = lu + (size_t)k * g.S;
             const double piv = __ldcg(uk + g.c);
             const double l = __ddiv_rn(row[s], piv);
@@ -196,33 +211,42 @@ box_ilu0_kernel(Geom g, double *lu, const uint32_t *__restrict__ mask, int *flag
             const int ylo = g.d > 1 ? max(g.r - sy, g.d == 2 ? g.r : 0) : 0;
             const int yhi = g.d > 1 ? min(g.W + g.r - sy, g.W) : 1;
             const int zlo = g.d > 2 ? max(g.r - sz, g.r) : 0, zhi = g.d > 2 ? min(g.W + g.r - sz, g.W) : 1;
-            // threads: lane along x, the rest along (y, z) pairs
+            // threads: lane along x, the rest along (y, z) pairs; the loads of one
+            // batch are all issued before any update uses them
+            constexpr int B = 16;
             const int nx = xhi - xlo;
-            const int lanes_x = 32;
-            const int tx = tid % lanes_x, tyz = tid / lanes_x, nyz_threads = TPR / lanes_x;
+            const int tx = tid & 31, tyz = tid >> 5, nyz_threads = TPR / 32;
             const int ny = yhi - ylo, nz = zhi - zlo;
             const int sxp = xlo + tx;
-            if (tx < nx) {
-                const int colx = kx + sxp - g.r;
-                const bool xok = colx >= 0 && colx < g.K;
-                for (int q = tyz; q < ny * nz; q += nyz_threads) {
+            const int colx = kx + sxp - g.r;
+            const bool xok = tx < nx && colx >= 0 && colx < g.K;
+            for (int q0 = tyz; q0 < ny * nz; q0 += nyz_threads * B) {
+                double u[B];
+                int tt[B];
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                    const int q = q0 + j * nyz_threads;
                     const int syp = g.d > 1 ? ylo + q % ny : g.r;
                     const int szp = g.d > 2 ? zlo + q / ny : g.r;
                     const int sp = sxp + (g.d > 1 ? g.W * syp : 0) + (g.d > 2 ? g.W * g.W * szp : 0);
-                    if (sp <= g.c || !xok) continue;
+                    bool ok = xok && q < ny * nz && sp > g.c;
                     if (g.d > 1) {
                         const int cy = ky + syp - g.r;
-                        if (cy < 0 || cy >= g.K) continue;
+                        ok = ok && cy >= 0 && cy < g.K;
                     }
                     if (g.d > 2) {
                         const int cz = kz + szp - g.r;
-                        if (cz < 0 || cz >= g.K) continue;
+                        ok = ok && cz >= 0 && cz < g.K;
                     }
                     const int t = (sx + sxp - g.r) + (g.d > 1 ? g.W * (sy + syp - g.r) : 0) +
                                   (g.d > 2 ? g.W * g.W * (sz + szp - g.r) : 0);
-                    if (!((bits[t >> 5] >> (t & 31)) & 1u)) continue;
-                    row[t] = __dsub_rn(row[t], __dmul_rn(l, __ldcg(uk + sp)));
+                    ok = ok && ((bits[t >> 5] >> (t & 31)) & 1u);
+                    u[j] = ok ? __ldcg(uk + sp) : 0.0;
+                    tt[j] = ok ? t : -1;
                 }
+#pragma unroll
+                for (int j = 0; j < B; ++j)
+                    if (tt[j] >= 0) row[tt[j]] = __dsub_rn(row[tt[j]], __dmul_rn(l, u[j]));
             }
             row_sync<TPR>();
         }
@@ -232,6 +256,180 @@ box_ilu0_kernel(Geom g, double *lu, const uint32_t *__restrict__ mask, int *flag
         if (tid == 0) {
             __threadfence();
             *((volatile int *)(flags + i)) = epoch;
+        }
+    }
+}
+
+// Line-pipelined ILU(0) for 1-D/2-D boxes.  A CTA owns one x-line at a time
+// (lines in natural order by ticket); its NW warps take the line's rows
+// round-robin, one row per warp in flight, each row double-buffered in shared
+// memory.  The row's last r elimination steps (the in-line slots, k = i-1..i-r)
+// are the critical path of the whole factorisation; they read the sibling rows'
+// finished U parts straight from shared memory.  Off-line steps read rows of
+// earlier lines through L2 once that line's published contiguous-prefix row
+// count covers them (flags[line], one relaxed poll per offset group).  Arithmetic and per-entry update order are exactly those of
+// box_ilu0_kernel (and of the reference), so the factors are identical.
+// Requires NW >= r + 1 (a row buffer is recycled only after every row that
+// reads it has finished) and 2 * NW * S doubles of shared memory.
+template <int NW>
+__global__ void __launch_bounds__(32 * NW)
+box_ilu0_line_kernel(Geom g, double *lu, const uint32_t *__restrict__ mask,
+                     const unsigned char *__restrict__ full, int *flags, int epoch, int *ticket,
+                     double tol, unsigned long long *bad) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ int s_rowdone[2 * NW];
+    __shared__ int s_prefix;
+    __shared__ int s_line;
+    volatile int *v_prefix = &s_prefix;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int K = g.K, r = g.r;
+    const int S = g.S, c = g.c;
+    const int mwS = (g.mw + 1) & ~1;                     // mask words, padded to 8 bytes
+    const int bufd = S + mwS / 2;                        // doubles per row buffer
+    volatile int *v_done = s_rowdone;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_line = atomicAdd(ticket, 1);
+        for (int q = tid; q < 2 * NW; q += blockDim.x) s_rowdone[q] = -1;
+        if (tid == 0) s_prefix = 0;
+        __syncthreads();
+        const int L = s_line;
+        if (L >= g.nlines) return;
+        const int iy = g.d > 1 ? L : 0;
+        const int64_t row0 = (int64_t)L * K;
+        for (int ix = warp, it = 0; ix < K; ix += NW, ++it) {
+            const int buf = (ix / NW) & 1;
+            double *row = sm + (size_t)(warp * 2 + buf) * bufd;
+            uint32_t *bits = reinterpret_cast<uint32_t *>(row + S);
+            const int64_t i = row0 + ix;
+            for (int q = lane; q < S; q += 32) row[q] = lu[(size_t)i * S + q];
+            for (int q = lane; q < g.mw; q += 32) bits[q] = mask[(size_t)i * g.mw + q];
+            __syncwarp();
+            // Elimination steps over the in-pattern lower slots, software
+            // pipelined: while step s updates the row, the flag check and the U
+            // loads of the next off-line step are already in flight (two
+            // register sets, ping-pong).  In-line steps read shared memory.
+            constexpr int B = 16;   // >= r + 1 rows of upper slots in 2-D
+            struct Step {
+                int s, sx, sy;
+                bool inl;
+                int64_t k;
+                double piv;
+                double u[B];
+                int tt[B];
+            };
+            auto next_slot = [&](int s0) {
+                for (int s1 = s0; s1 < c; ++s1)
+                    if ((bits[s1 >> 5] >> (s1 & 31)) & 1u) return s1;
+                return c;
+            };
+            // gather row k's upper entries that land in row i's pattern
+            const bool full_i = full[i] != 0;
+            auto gather = [&](Step &st, const double *uk, bool shared) {
+                if (full_i && full[st.k]) {
+                    // every slot of rows i and k is in the pattern: the targets are
+                    // t = s' + s - c, no boundary or pattern tests needed
+                    const int xlo = max(r - st.sx, 0), xhi = min(g.W + r - st.sx, g.W);
+                    const int ylo = g.d > 1 ? max(r - st.sy, r) : 0;
+                    const int yhi = g.d > 1 ? min(g.W + r - st.sy, g.W) : 1;
+                    const int sxp = xlo + lane;
+                    const bool xok = lane < xhi - xlo;
+                    const int shift = st.s - c;
+                    st.piv = shared ? uk[c] : __ldcg(uk + c);
+#pragma unroll
+                    for (int j = 0; j < B; ++j) {
+                        const int sp = sxp + g.W * (ylo + j);
+                        const bool ok = xok && ylo + j < yhi && sp > c;
+                        st.u[j] = ok ? (shared ? uk[sp] : __ldcg(uk + sp)) : 0.0;
+                        st.tt[j] = ok ? sp + shift : -1;
+                    }
+                    return;
+                }
+                const int kx = ix + st.sx - r, ky = iy + st.sy - r;
+                const int xlo = max(r - st.sx, 0), xhi = min(g.W + r - st.sx, g.W);
+                const int ylo = g.d > 1 ? max(r - st.sy, r) : 0;
+                const int yhi = g.d > 1 ? min(g.W + r - st.sy, g.W) : 1;
+                const int nx = xhi - xlo, ny = yhi - ylo;
+                const int sxp = xlo + lane;
+                const int colx = kx + sxp - r;
+                const bool xok = lane < nx && colx >= 0 && colx < K;
+                st.piv = shared ? uk[c] : __ldcg(uk + c);
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                    const int syp = g.d > 1 ? ylo + j : r;
+                    const int sp = sxp + (g.d > 1 ? g.W * syp : 0);
+                    bool ok = xok && j < ny && sp > c;
+                    if (g.d > 1) {
+                        const int cy = ky + syp - r;
+                        ok = ok && cy >= 0 && cy < K;
+                    }
+                    const int t = (st.sx + sxp - r) + (g.d > 1 ? g.W * (st.sy + syp - r) : 0);
+                    ok = ok && ((bits[t >> 5] >> (t & 31)) & 1u);
+                    st.u[j] = ok ? (shared ? uk[sp] : __ldcg(uk + sp)) : 0.0;
+                    st.tt[j] = ok ? t : -1;
+                }
+            };
+            // decode slot s; for an off-line step wait for row k and issue its loads
+            // Earlier lines publish a contiguous-prefix row count; the rows of
+            // line L + oy this row needs are those with x <= ix + r, checked once
+            // per offset group oy.
+            int oy_ready = -1 << 20;
+            auto prepare = [&](Step &st, int s) {
+                st.s = s;
+                if (s >= c) return;
+                st.sx = s % g.W;
+                st.sy = g.d > 1 ? s / g.W : r;
+                st.inl = st.sy == r;
+                st.k = i + (st.sx - r) + (int64_t)K * (st.sy - r);
+                if (!st.inl) {
+                    if (st.sy != oy_ready) {
+                        const int need = min(K, ix + r + 1);
+                        while (ld_flag(flags + (L + st.sy - r)) < need) {
+                        }
+                        oy_ready = st.sy;
+                    }
+                    gather(st, lu + (size_t)st.k * S, false);
+                }
+            };
+            auto execute = [&](Step &st) {
+                if (st.inl) {
+                    const int kix = ix - (r - st.sx);
+                    while (v_done[kix % (2 * NW)] != kix) {
+                    }
+                    gather(st, sm + (size_t)((kix % NW) * 2 + ((kix / NW) & 1)) * bufd, true);
+                }
+                const double l = __ddiv_rn(row[st.s], st.piv);
+                if (lane == 0 && fabs(st.piv) < tol)
+                    atomicMin(bad, (unsigned long long)(i * g.n + st.k));
+#pragma unroll
+                for (int j = 0; j < B; ++j)
+                    if (st.tt[j] >= 0) row[st.tt[j]] = __dsub_rn(row[st.tt[j]], __dmul_rn(l, st.u[j]));
+                __syncwarp();
+                if (lane == 0) row[st.s] = l;     // no later step touches slot s
+                __syncwarp();
+            };
+            Step A, Bq;
+            prepare(A, next_slot(0));
+            while (A.s < c) {
+                prepare(Bq, next_slot(A.s + 1));
+                execute(A);
+                if (Bq.s >= c) break;
+                prepare(A, next_slot(Bq.s + 1));
+                execute(Bq);
+            }
+            for (int q = lane; q < S; q += 32) __stcg(lu + (size_t)i * S + q, row[q]);
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) {
+                v_done[ix % (2 * NW)] = ix;
+                // publish the line's contiguous prefix in row order
+                while (*v_prefix != ix) {
+                }
+                __threadfence();
+                *((volatile int *)(flags + L)) = ix + 1;
+                *v_prefix = ix + 1;
+            }
+            __syncwarp();
         }
     }
 }
@@ -303,7 +501,32 @@ int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st) {
     LP_CUDA(cudaGetDevice(&dev));
     int nsm = 148;
     LP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    if (g.S <= 1200) {
+    constexpr int LNW = 16;
+    const size_t line_smem = (size_t)2 * LNW * (g.S + ((g.mw + 1) & ~1) / 2) * sizeof(double);
+    // The row-ticket kernel keeps ~(resident CTAs) rows in flight in natural
+    // order; that window must span the wavefront, about K (r + 1) rows.  When
+    // it does not (long lines), the line-pipelined kernel is used instead.
+    // (Measured on B200: cfg 2, K (r+1) = 3315 -> row kernel 57 ms vs line kernel
+    // 198 ms; cfg 3, K (r+1) = 30705 -> row kernel 9.5 s vs line kernel 3.1 s.)
+    const bool window_ok = (int64_t)g.K * (g.r + 1) <= 8192;
+    if (g.d <= 2 && !window_ok && g.r + 1 <= LNW && line_smem <= 220 * 1024) {
+        LP_CUDA(cudaFuncSetAttribute(box_ilu0_line_kernel<LNW>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)line_smem));
+        int occ = 1;
+        LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, box_ilu0_line_kernel<LNW>,
+                                                              32 * LNW, line_smem));
+        int64_t blocks = (int64_t)occ * nsm;
+        if (blocks > g.nlines) blocks = g.nlines;
+        unsigned char *full = nullptr;
+        int rcf;
+        if ((rcf = dalloc(&full, (size_t)b.n, "full-row flags"))) return rcf;
+        box_full_kernel<<<148 * 8, 256, 0, st>>>(g, b.mask, full);
+        box_ilu0_line_kernel<LNW><<<(unsigned)blocks, 32 * LNW, line_smem, st>>>(
+            g, b.lu, b.mask, full, m->flags, epoch, m->ticket, tol, key);
+        count_launch();
+        LP_CUDA(cudaStreamSynchronize(st));
+        dfree(full);
+    } else if (g.S <= 1200) {
         LP_CUDA(cudaFuncSetAttribute(box_ilu0_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         int occ = 1;
@@ -430,9 +653,9 @@ extern "C" int lp_box_assemble(int d, int K, int n_groups, const int *lens, cons
     unsigned long long *cnt = nullptr;
     const size_t nblk = (size_t)2 * (tmax + 1) * (2 * a.R + 1) * K;
     auto fail = [&](int code) {
-        if (dhats) cudaFree(dhats);
-        if (dblocks) cudaFree(dblocks);
-        if (cnt) cudaFree(cnt);
+        if (dhats) dfree(dhats);
+        if (dblocks) dfree(dblocks);
+        if (cnt) dfree(cnt);
         lp_ilu_destroy(m);
         return code;
     };
@@ -468,9 +691,9 @@ extern "C" int lp_box_assemble(int d, int K, int n_groups, const int *lens, cons
     e = cudaMemcpy(host, cnt, sizeof host, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail(cuda_fail(e, "assembly", __FILE__, __LINE__));
     LP_CUDA(cudaMemset(m->flags, 0, b.n * sizeof(int)));
-    cudaFree(dhats);
-    cudaFree(dblocks);
-    cudaFree(cnt);
+    dfree(dhats);
+    dfree(dblocks);
+    dfree(cnt);
     b.nnz = (int64_t)host[0];
     m->nnz = b.nnz;
     if (b.nnz == 0) {

@@ -250,11 +250,12 @@ extern "C" int lp_csr_create(int64_t n, int64_t nnz, const int64_t *indptr,
 
 extern "C" int lp_ilu_destroy(lp_ilu *m) {
     if (!m) return LP_OK;
+    cudaDeviceSynchronize();
     void *ptrs[] = {m->indptr, m->indices, m->values, m->lu, m->diag, m->flags, m->ticket,
                     m->bad, m->ytmp, m->box.values, m->box.lu, m->box.mask,
                     m->box.band_lo, m->box.band_up, m->box.diag};
     for (void *p : ptrs)
-        if (p) cudaFree(p);
+        if (p) dfree(p);
     delete m;
     return LP_OK;
 }

@@ -306,7 +306,7 @@ int line_table_build(LineTable &t, const double *Tdev, int P, int nk, int ps,
 void line_table_free(LineTable &t) {
     double **ps[] = {&t.u_sym, &t.u_anti, &t.u_mid, &t.f_even, &t.f_odd, &t.f_mid_e, &t.f_mid_o};
     for (double **p : ps) {
-        if (*p) cudaFree(*p);
+        if (*p) dfree(*p);
         *p = nullptr;
     }
 }

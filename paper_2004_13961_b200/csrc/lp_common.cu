@@ -23,17 +23,41 @@ int cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
     return e == cudaErrorMemoryAllocation ? LP_ERR_OOM : LP_ERR_CUDA;
 }
 
+// Library buffers come from the device's default stream-ordered memory pool
+// with an unbounded release threshold, so the per-solve factor and workspace
+// buffers (hundreds of MB) are recycled instead of hitting cudaMalloc/cudaFree
+// (which also synchronise the device) on every pcg_solve.
+static void init_pool() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t threshold = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+    cudaGetLastError();
+    done = true;
+}
+
 int dalloc(void **p, size_t bytes, const char *what) {
     *p = nullptr;
     if (bytes == 0) bytes = 8;
-    cudaError_t e = cudaMalloc(p, bytes);
+    init_pool();
+    cudaError_t e = cudaMallocAsync(p, bytes, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
     if (e != cudaSuccess) {
         cudaGetLastError();
+        *p = nullptr;
         set_error("device allocation of %zu bytes for %s failed: %s", bytes, what,
                   cudaGetErrorString(e));
         return LP_ERR_OOM;
     }
     return LP_OK;
+}
+
+void dfree(void *p) {
+    if (p) cudaFreeAsync(p, 0);
 }
 
 }  // namespace lp

@@ -34,6 +34,9 @@ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 // Device allocation that records an LP_ERR_OOM message on failure.
 int dalloc(void **p, size_t bytes, const char *what);
+// Release a dalloc'd buffer (stream-ordered on the legacy stream; callers that
+// may still have work in flight on other streams synchronise first).
+void dfree(void *p);
 template <class T>
 int dalloc(T **p, size_t count, const char *what) {
     return dalloc(reinterpret_cast<void **>(p), count * sizeof(T), what);

@@ -106,7 +106,7 @@ int device_min(const double *v, int64_t n, double *result, cudaStream_t st) {
     double hostp[blocks];
     cudaError_t e = cudaMemcpyAsync(hostp, part, sizeof hostp, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    cudaFree(part);
+    dfree(part);
     LP_CUDA(e);
     double m = INFINITY;
     for (int i = 0; i < blocks; ++i) m = fmin(m, hostp[i]);
@@ -142,7 +142,7 @@ extern "C" int lp_plan_create(int P, const double *nodes, const double *weights,
         e = cudaMemcpy(p->weights, weights, P * sizeof(double), cudaMemcpyDefault);
     if (e != cudaSuccess) {
         lp_plan_destroy(p);
-        cudaFree(Phi); cudaFree(DPhi); cudaFree(Tf);
+        dfree(Phi); dfree(DPhi); dfree(Tf);
         return cuda_fail(e, "plan upload", __FILE__, __LINE__);
     }
     vandermonde_kernel<<<(P + 127) / 128, 128, 0, st>>>(P, p->nodes, V);
@@ -153,14 +153,14 @@ extern "C" int lp_plan_create(int P, const double *nodes, const double *weights,
         (rc = line_table_build(p->tF, Tf, P, P, 0, st)) ||
         (P >= 4 && (rc = line_table_build(p->tPhi, Phi, P, P - 2, 0, st))) ||
         (P >= 4 && (rc = line_table_build(p->tDPhi, DPhi, P, P - 2, 1, st)))) {
-        cudaFree(Phi); cudaFree(DPhi); cudaFree(Tf);
+        dfree(Phi); dfree(DPhi); dfree(Tf);
         lp_plan_destroy(p);
         return rc;
     }
     e = cudaDeviceSynchronize();
-    cudaFree(Phi);
-    cudaFree(DPhi);
-    cudaFree(Tf);
+    dfree(Phi);
+    dfree(DPhi);
+    dfree(Tf);
     if (e != cudaSuccess) {
         lp_plan_destroy(p);
         return cuda_fail(e, "plan tables", __FILE__, __LINE__);
@@ -171,13 +171,14 @@ extern "C" int lp_plan_create(int P, const double *nodes, const double *weights,
 
 extern "C" int lp_plan_destroy(lp_plan *p) {
     if (!p) return LP_OK;
+    cudaDeviceSynchronize();
     line_table_free(p->tV);
     line_table_free(p->tF);
     line_table_free(p->tPhi);
     line_table_free(p->tDPhi);
-    if (p->nodes) cudaFree(p->nodes);
-    if (p->weights) cudaFree(p->weights);
-    if (p->V) cudaFree(p->V);
+    if (p->nodes) dfree(p->nodes);
+    if (p->weights) dfree(p->weights);
+    if (p->V) dfree(p->V);
     delete p;
     return LP_OK;
 }
@@ -243,7 +244,7 @@ extern "C" int lp_operator_create(lp_plan *plan, int d, const double *beta_grid,
     double *stage = nullptr;
     if ((rc = dalloc(&stage, nP, "grid staging"))) { delete op; return rc; }
     cudaStream_t st = 0;
-    auto fail = [&](int code) { cudaFree(stage); lp_operator_destroy(op); return code; };
+    auto fail = [&](int code) { dfree(stage); lp_operator_destroy(op); return code; };
     for (int g = 0; g < ngrids; ++g) {
         if ((rc = dalloc(&op->beta_w[g], nP, "weighted beta grid"))) return fail(rc);
         const double *src = n_axis_betas ? axis_betas[g] : beta_grid;
@@ -274,7 +275,7 @@ extern "C" int lp_operator_create(lp_plan *plan, int d, const double *beta_grid,
         (rc = dalloc(&op->wsB, 3 * nP, "operator workspace")))
         return fail(rc);
     cudaError_t e = cudaDeviceSynchronize();
-    cudaFree(stage);
+    dfree(stage);
     if (e != cudaSuccess) {
         lp_operator_destroy(op);
         return cuda_fail(e, "operator setup", __FILE__, __LINE__);
@@ -285,11 +286,12 @@ extern "C" int lp_operator_create(lp_plan *plan, int d, const double *beta_grid,
 
 extern "C" int lp_operator_destroy(lp_operator *op) {
     if (!op) return LP_OK;
+    cudaDeviceSynchronize();
     for (int g = 0; g < op->n_beta_grids; ++g)
-        if (op->beta_w[g]) cudaFree(op->beta_w[g]);
-    if (op->alpha_w) cudaFree(op->alpha_w);
-    if (op->wsA) cudaFree(op->wsA);
-    if (op->wsB) cudaFree(op->wsB);
+        if (op->beta_w[g]) dfree(op->beta_w[g]);
+    if (op->alpha_w) dfree(op->alpha_w);
+    if (op->wsA) dfree(op->wsA);
+    if (op->wsB) dfree(op->wsB);
     delete op;
     return LP_OK;
 }

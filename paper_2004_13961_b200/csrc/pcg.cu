@@ -27,7 +27,7 @@ struct Workspace {
     ~Workspace() {
         double *ps[] = {r, z, p, w, partial, scal};
         for (double *q : ps)
-            if (q) cudaFree(q);
+            if (q) dfree(q);
         if (host) cudaFreeHost(host);
     }
 };
