@@ -143,6 +143,24 @@ def dgemm_tflops(torch):
     return 2.0 * n ** 3 / best / 1e12
 
 
+def sweep_traffic(workload):
+    """DRAM bytes (read + write) of one precond_apply (two box_sweep_kernel launches)
+    from the committed ncu --set full capture (profiles/r01_box_sweep_full.csv, cfg 2)."""
+    if workload != "cfg2":
+        return None
+    path = os.path.join(ROOT, "profiles", "r01_box_sweep_full.csv")
+    try:
+        import csv
+        tot = 0.0
+        with open(path) as f:
+            for row in csv.reader(f):
+                if row and row[0].startswith("void") and "box_sweep_kernel" in row[0]:
+                    tot += (float(row[2]) + float(row[3])) * 1e6
+        return tot or None
+    except (OSError, ValueError, IndexError):
+        return None
+
+
 def flush_l2(torch, buf):
     buf.zero_()
 
@@ -275,9 +293,9 @@ def run_b200(args, ws, rank, local):
               "loop_s_per_iter": loop_per_iter, "nnz_M": nnz}
     share = {"ilu0": t_fac, "sweeps": t_sweep * iters, "matvec": t_mv * iters}
     dom = max(share, key=share.get)
-    roof_sweep = {"kernel": "box_fwd+box_bwd (precond_apply)", "bound": "hbm",
+    roof_sweep = {"kernel": "box_sweep_kernel fwd+bwd (precond_apply)", "bound": "hbm",
                   "achieved": sw_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                  "frac": sw_gbs / peaks["hbm_gbs"], "traffic": None,
+                  "frac": sw_gbs / peaks["hbm_gbs"], "traffic": sweep_traffic(w.name),
                   "algorithmic_bytes": B_sw, "peak_source": peaks_kind}
     roof_mv = {"kernel": "line_transform_kernel x4 (apply_system)", "bound": "fp64",
                "achieved": mv_tf, "peak": fp64, "unit": "TFLOP/s", "frac": mv_tf / fp64,
