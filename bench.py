@@ -154,8 +154,8 @@ def sweep_traffic(workload):
         tot = 0.0
         with open(path) as f:
             for row in csv.reader(f):
-                if row and row[0].startswith("void") and "box_sweep_kernel" in row[0]:
-                    tot += (float(row[2]) + float(row[3])) * 1e6
+                if row and "box_sweep_kernel" in row[0]:
+                    tot += (float(row[2]) + float(row[3])) * 1e6   # Mbyte
         return tot or None
     except (OSError, ValueError, IndexError):
         return None
