@@ -154,7 +154,7 @@ def sweep_traffic(workload):
         tot = 0.0
         with open(path) as f:
             for row in csv.reader(f):
-                if row and "box_sweep_kernel" in row[0]:
+                if len(row) >= 4 and "box_sweep_kernel" in row[0] and not row[0].startswith("#"):
                     tot += (float(row[2]) + float(row[3])) * 1e6   # Mbyte
         return tot or None
     except (OSError, ValueError, IndexError):
