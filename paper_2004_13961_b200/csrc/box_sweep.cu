@@ -3,27 +3,31 @@
 //
 // A CTA owns one x-line at a time (lines handed out in sweep order by an
 // atomic ticket, so a CTA only ever waits on lines owned by running CTAs).
-// Per line:
-//  * producer warps (all but the serial warp) take rows round-robin.  Each keeps the next
-//    row's off-line factor entries in flight (register double buffer), gathers
-//    the solution values those entries multiply and reduces
-//    c_i = rhs_i - sum L_is y_col(s) into a shared ring;
-//  * the serial warp runs the in-line recurrence
-//        y_i = c_i - sum_{q=1..r} L_{i,i-q} y_{i-q}
-//    "right-looking": lane q carries the partial sum of row i+q, so a row
-//    costs one broadcast, one lane shift and one FMA per lane.  The in-line
-//    band values are staged from a compact band array into a shared ring by
-//    cp.async (register prefetch queues get their registers reused as
-//    temporaries by the compiler, which serialises every step on the load).
+// Row t of line L needs, besides its own line, the rows x <= t + r of the
+// earlier lines of its stencil.  The work of a line is split so that the
+// line-to-line critical path carries as little as possible:
 //
-// Synchronisation carries no fences at all: every value is its own flag.
-// The output vector is pre-filled with a NaN sentinel; a consumer spins on the
-// 8-byte value it needs (aligned 64-bit accesses are single-copy atomic, and
-// the loads/stores are .cg, i.e. coherent at L2) until it is no longer the
-// sentinel.  The same trick, with per-step sentinels, carries the shared ring.
-// Computed NaNs are canonicalised so they can never alias a sentinel.  The
-// backward sweep is the mirror image (rows and lines in reverse, division by
-// the diagonal).
+//  * the serial warp owns everything that depends on the immediately
+//    preceding line L-1 (the 2r+1 entries with offset oy = -1, oz = 0) and on
+//    the line itself (the r in-line entries).  Lane k carries the running sum
+//    of row t+k (k <= 2r).  Each step polls the one new value y(L-1, t+r) and
+//    folds it into all 2r+1 running sums, adds y_{t-1} to the in-line sums,
+//    and lane 0 finishes y_t = (c_t - A_t) - l1_t y_{t-1}: a line can trail
+//    its predecessor by only ~r steps plus one L2 round trip;
+//  * producer warps take rows round-robin and reduce the rest of the stencil
+//    (lines L-2 and older, previous planes), which was produced long before:
+//    c_t = rhs_t - sum L_ts y_col(s), into a shared ring, with the next row's
+//    factor loads in flight (two register sets, ping-pong).
+//
+// Synchronisation carries no fences: every value is its own flag.  The output
+// vector is pre-filled with a NaN sentinel; a consumer polls the 8-byte value
+// it needs (aligned 64-bit accesses are single-copy atomic; relaxed .gpu
+// loads, coherent at L2) until it is no longer the sentinel.  The shared ring
+// uses per-step sentinels; computed NaNs are canonicalised so they can never
+// alias a sentinel.  Band coefficients are staged by cp.async (register
+// prefetch queues get their registers reused by the compiler, serialising
+// every step on the load).  The backward sweep is the mirror image (rows and
+// lines in reverse, scaling by 1/U_tt).
 #include <math.h>
 
 #include "box_geom.cuh"
@@ -38,17 +42,12 @@ constexpr unsigned long long SWEEP_SENTINEL = 0xFFF4C0FFEE5EED00ull;   // signal
 
 namespace {
 
-constexpr int RING = 64;   // rows in flight per line (power of two)
+constexpr int RING = 64;    // rows in flight per line (power of two)
 constexpr int BRING = 128;  // band rows staged for the serial warp (power of two)
 constexpr unsigned long long RING_SENT = 0xFFF5000000000000ull;
 
 #ifndef LP_SWEEP_SLEEP
 #define LP_SWEEP_SLEEP 20
-#endif
-#if LP_SWEEP_SLEEP > 0
-#define LP_BACKOFF() __nanosleep(LP_SWEEP_SLEEP)
-#else
-#define LP_BACKOFF() do {} while (0)
 #endif
 
 __device__ __forceinline__ unsigned long long bits(double v) {
@@ -59,32 +58,12 @@ __device__ __forceinline__ double canon(double v) {
     return isnan(v) ? __longlong_as_double(0x7FF8000000000000ll) : v;
 }
 
-// Relaxed gpu-scope load that the compiler may neither cache nor elide
-// (a plain .cg load in a side-effect-free spin loop can legally be removed).
+// Relaxed gpu-scope load that the compiler may neither cache nor elide (a
+// plain load in a side-effect-free spin loop can legally be removed).
 __device__ __forceinline__ double ld_poll(const double *p) {
     double v;
     asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
     return v;
-}
-
-#ifndef LP_SWEEP_PUBMODE
-#define LP_SWEEP_PUBMODE 2
-#endif
-// Publish a solution value to other SMs.  A plain .cg store can linger in the
-// SM's write path for microseconds; an L2-performed reduction is visible as
-// soon as it reaches L2.  The slot holds the sentinel, so xor-ing in
-// (sentinel ^ value) leaves exactly the value.
-__device__ __forceinline__ void publish(double *p, double y) {
-#if LP_SWEEP_PUBMODE == 0
-    __stcg(p, y);
-#elif LP_SWEEP_PUBMODE == 1
-    atomicExch(reinterpret_cast<unsigned long long *>(p), bits(y));
-#elif LP_SWEEP_PUBMODE == 2
-    const unsigned long long x = bits(y) ^ SWEEP_SENTINEL;
-    asm volatile("red.relaxed.gpu.global.xor.b64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
-#else
-    asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(y) : "memory");
-#endif
 }
 
 __device__ __forceinline__ double ring_sent(int t) {
@@ -97,12 +76,26 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
 struct SweepArgs {
     Geom g;
-    const double *lu, *band, *diag, *rhs;
+    const double *lu;     // factors [n][S]
+    const double *band;   // [n][bs]: r in-line coefficients, then the 2r+1 of line L-/+1
+    const double *rdiag;  // 1/U_tt
+    const double *rhs;
     double *out;
     int *ticket;
-    int lo, nslot;   // off-line slot range [lo, lo + nslot)
+    int bs;               // band row stride (even)
+    int lo, nslot;        // producers' slot range [lo, lo + nslot)
     unsigned long long *trace;   // LP_SWEEP_TRACE builds: per-line timestamps
 };
 
@@ -117,26 +110,27 @@ __global__ void __launch_bounds__(32 * NW)
 box_sweep_kernel(const __grid_constant__ SweepArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const Geom &g = a.g;
-    int *s_delta = reinterpret_cast<int *>(dsm);
+    double *s_band = reinterpret_cast<double *>(dsm);                  // [BRING][bs]
+    double *s_rd = s_band + (size_t)BRING * a.bs;                       // [BRING]
+    int *s_delta = reinterpret_cast<int *>(s_rd + BRING);               // [nslot]
     signed char *s_ox = reinterpret_cast<signed char *>(s_delta + a.nslot);
     signed char *s_oy = s_ox + a.nslot;
     signed char *s_oz = s_oy + a.nslot;
     unsigned char *s_ok = reinterpret_cast<unsigned char *>(s_oz + a.nslot);
     __shared__ double s_c[RING];
-    __shared__ __align__(16) double s_band[BRING * 30];   // serial warp's band ring
-    __shared__ double s_rd[BRING];                         // 1/U_tt ring (backward)
     __shared__ int s_line;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int K = g.K, r = g.r;
     volatile double *v_c = s_c;
+    constexpr int SERIAL = NW - 1;   // highest warp id: favoured by the SMSP arbiter
 
     for (int j = tid; j < a.nslot; j += blockDim.x) {
         int sx, sy, sz;
         slot_axes(g, a.lo + j, sx, sy, sz);
-        s_ox[j] = (signed char)(sx - g.r);
-        s_oy[j] = (signed char)(sy - g.r);
-        s_oz[j] = (signed char)(sz - g.r);
-        s_delta[j] = (sx - g.r) + K * ((sy - g.r) + K * (sz - g.r));
+        s_ox[j] = (signed char)(sx - r);
+        s_oy[j] = (signed char)(sy - r);
+        s_oz[j] = (signed char)(sz - r);
+        s_delta[j] = (sx - r) + K * ((sy - r) + K * (sz - r));
     }
 
     for (;;) {
@@ -153,138 +147,140 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
             s_ok[j] = (g.d < 2 || (y >= 0 && y < K)) && (g.d < 3 || (z >= 0 && z < K));
         }
         const int64_t row0 = (int64_t)L * K;
-        // The lex-latest line of the stencil in each earlier plane-row: once its
-        // value at the frontier x is visible, the row's whole stencil has almost
-        // certainly been produced (per-value sentinel checks remain the guard).
-        int dep1, dep2;
-        if (FWD) {
-            dep1 = (g.d > 1 && iy > 0) ? L - 1 : -1;
-            dep2 = (g.d > 2 && iz > 0) ? min(iy + r, K - 1) + K * (iz - 1) : -1;
-        } else {
-            dep1 = (g.d > 1 && iy < K - 1) ? L + 1 : -1;
-            dep2 = (g.d > 2 && iz < K - 1) ? max(iy - r, 0) + K * (iz + 1) : -1;
-        }
 #ifdef LP_SWEEP_TRACE
         if (tid == 0 && a.trace) a.trace[(size_t)tl * 4] = gtime();
 #endif
         __syncthreads();
 
-        // The serial warp is the highest-numbered one: the SMSP arbiter issues
-        // highest-warp-id first, so it wins every slot it is eligible for.
-#ifndef LP_SWEEP_SERIAL_WARP
-#define LP_SWEEP_SERIAL_WARP (NW - 1)
-#endif
-        if (warp == LP_SWEEP_SERIAL_WARP) {
+        if (warp == SERIAL) {
             // ------------------------------------------- serial recurrence
-            // Lane 0 carries the scalar chain y_t = (c_t - A_t) - l1_t y_{t-1}
-            // (one FMA per row on the critical path; backward also scales by
-            // 1/U_tt).  Lane k >= 1 holds A_{t+k} = sum_{q>=2} L_{t+k,t+k-q} y_{t+k-q}
-            // and adds y_{t-1} one step after it is produced; a lane shift then
-            // hands A_{t+1} to lane 0.  Lane k's coefficient for step t is
-            // band[row(t+k)][k] (lane 0: l1_t).  The band rows are staged into a
-            // shared ring by cp.async, two 32-row chunks ahead.
-            // Band rows live in the ring by memory row (ix mod BRING), r doubles
-            // each; 1/U_tt in a separate ring.  A chunk = 32 steps = 32 rows,
-            // contiguous in memory, copied with 16-byte cp.async when 16-byte
-            // aligned (r even), else 8-byte.
-            const bool vec16 = (r % 2) == 0;
+            const bool has_prev = g.d > 1 && (FWD ? iy > 0 : iy < K - 1);
+            const double *prev = a.out + (FWD ? row0 - K : row0 + K);   // line L-/+1
+            const int LW = g.d > 1 ? 2 * r : r - 1;   // lanes >= LW hold no pending sum
+            auto ix_of = [&](int t) { return FWD ? t : K - 1 - t; };
+            // band rows of steps [u0, u0+32), contiguous in memory, by ix mod BRING
             auto stage_chunk = [&](int u0) {
                 if (u0 < K) {
                     const int u1 = min(u0 + 32, K);
-                    const int ixlo = FWD ? u0 : K - u1, ixhi = FWD ? u1 : K - u0;   // [ixlo, ixhi)
-                    // split at the ring wrap so each piece is contiguous in smem
+                    const int ixlo = FWD ? u0 : K - u1, ixhi = FWD ? u1 : K - u0;
                     for (int p0 = ixlo; p0 < ixhi;) {
                         const int p1 = min(ixhi, (p0 / BRING + 1) * BRING);
-                        const double *src = a.band + (size_t)(row0 + p0) * r;
-                        double *dst = s_band + (size_t)(p0 & (BRING - 1)) * r;
-                        const int n = (p1 - p0) * r;
-                        if (vec16) {
-                            for (int e = 2 * lane; e < n; e += 64) {
-                                const unsigned d = (unsigned)__cvta_generic_to_shared(dst + e);
-                                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d),
-                                             "l"(src + e) : "memory");
-                            }
-                        } else {
-                            for (int e = lane; e < n; e += 32) {
-                                const unsigned d = (unsigned)__cvta_generic_to_shared(dst + e);
-                                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d),
-                                             "l"(src + e) : "memory");
-                            }
-                        }
+                        const double *src = a.band + (size_t)(row0 + p0) * a.bs;
+                        double *dst = s_band + (size_t)(p0 & (BRING - 1)) * a.bs;
+                        const int n = (p1 - p0) * a.bs;
+                        for (int e = 2 * lane; e < n; e += 64) cp_async16(dst + e, src + e);
                         if (!FWD)
-                            for (int e = lane; e < p1 - p0; e += 32) {
-                                const unsigned d = (unsigned)__cvta_generic_to_shared(
-                                    s_rd + ((p0 + e) & (BRING - 1)));
-                                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d),
-                                             "l"(a.diag + row0 + p0 + e) : "memory");
-                            }
+                            for (int e = lane; e < p1 - p0; e += 32)
+                                cp_async8(s_rd + ((p0 + e) & (BRING - 1)), a.rdiag + row0 + p0 + e);
                         p0 = p1;
                     }
                 }
                 asm volatile("cp.async.commit_group;" ::: "memory");
             };
+            // lane k's two coefficients for step t (row t+k):
+            //   qi: in-line, multiplies y_{t-1} (lane 0: l1_t)
+            //   qg: line L-/+1, multiplies the step's new value y(L-/+1, t -/+ r)
+            auto coefs = [&](int t, double &qi, double &qg) {
+                const int tk = t + lane;
+                qi = 0.0;
+                qg = 0.0;
+                if (tk < 0 || tk >= K) return;
+                const double *b = s_band + (size_t)(ix_of(tk) & (BRING - 1)) * a.bs;
+                if (lane < r) qi = b[lane];
+                if (g.d > 1 && lane <= 2 * r) qg = b[r + (FWD ? 2 * r - lane : lane)];
+            };
+            auto xnew_of = [&](int t) { return FWD ? t + r : K - 1 - t - r; };
+            auto fetch_new = [&](int t) -> double {
+                const int x = xnew_of(t);
+                return (has_prev && x >= 0 && x < K) ? ld_poll(prev + x) : 0.0;
+            };
+            auto ready_new = [&](int t, double v) -> double {
+                const int x = xnew_of(t);
+                if (!has_prev || x < 0 || x >= K) return 0.0;
+                while (bits(v) == SWEEP_SENTINEL) v = ld_poll(prev + x);
+                return v;
+            };
+
             stage_chunk(0);
             stage_chunk(32);
+            stage_chunk(64);
+            asm volatile("cp.async.wait_group 2;" ::: "memory");
+            __syncwarp();
             double acc = 0.0, yprev = 0.0;
-            // The next step's c is read one step ahead by all lanes (a uniform,
-            // non-divergent poll); a divergent single-lane spin costs ~280 cycles.
+            double ynext = fetch_new(g.d > 1 ? -r : 0);
+            // virtual steps t = -r..-1: values of line L-/+1 at x < r (x > K-1-r)
+            if (g.d > 1)
+                for (int t = -r; t < 0; ++t) {
+                    double qi, qg;
+                    coefs(t, qi, qg);
+                    const double yn = ready_new(t, ynext);
+                    ynext = fetch_new(t + 1);
+                    acc = fma(qg, yn, acc);
+                    acc = __shfl_down_sync(0xffffffff, acc, 1);
+                    if (lane >= LW) acc = 0.0;
+                }
             double cn = v_c[0];
             for (int t0 = 0; t0 < K; t0 += 32) {
-                stage_chunk(t0 + 64);
-                asm volatile("cp.async.wait_group 1;" ::: "memory");
+                stage_chunk(t0 + 96);
+                asm volatile("cp.async.wait_group 2;" ::: "memory");
                 __syncwarp();
                 const int tend = min(t0 + 32, K);
                 for (int t = t0; t < tend; ++t) {
                     const int slot = t & (RING - 1);
-                    const int ixq = FWD ? t + lane : K - 1 - t - lane;
-                    const double qv = (lane < r && t + lane < K)
-                                          ? s_band[(ixq & (BRING - 1)) * r + lane] : 0.0;
+                    double qi, qg;
+                    coefs(t, qi, qg);
+                    const double yn = ready_new(t, ynext);
+                    ynext = fetch_new(t + 1);
                     const double yb = __shfl_sync(0xffffffff, yprev, 0);
-                    if (lane != 0) acc = fma(qv, yb, acc);
+                    acc = fma(qg, yn, acc);
+                    if (lane != 0) acc = fma(qi, yb, acc);
+                    // c_t from the producers, read one step ahead by all lanes
                     double cc = cn;
                     const unsigned long long sb = bits(ring_sent(t));
                     if (bits(cc) == sb) {
                         do {
-#ifdef LP_SWEEP_SERIAL_SLEEP
-                            __nanosleep(LP_SWEEP_SERIAL_SLEEP);
-#endif
                             cc = v_c[slot];
                         } while (bits(cc) == sb);
                     }
-                    double y = fma(-qv, yprev, cc - acc);
-                    if (!FWD) y *= s_rd[(K - 1 - t) & (BRING - 1)];
+                    double y = fma(-qi, yprev, cc - acc);
+                    if (!FWD) y *= s_rd[ix_of(t) & (BRING - 1)];
                     y = canon(y);
                     if (lane == 0) {
                         v_c[slot] = ring_sent(t + RING);
-                        publish(a.out + row0 + (FWD ? t : K - 1 - t), y);
+                        __stcg(a.out + row0 + ix_of(t), y);
                     }
 #ifdef LP_SWEEP_TRACE
                     if (lane == 0 && a.trace && (t == 0 || t == K / 2 || t == K - 1))
                         a.trace[(size_t)tl * 4 + (t == 0 ? 1 : (t == K - 1 ? 3 : 2))] = gtime();
 #endif
-#ifdef LP_SWEEP_TRACE
-                    if (lane == 0 && a.trace && (tl == g.nlines / 2 - 1 || tl == g.nlines / 2))
-                        a.trace[(size_t)g.nlines * 4 + (size_t)(tl == g.nlines / 2 - 1 ? 0 : 1) * K * 6 +
-                                (size_t)t * 6 + 3] = gtime();
-#endif
                     cn = v_c[(t + 1) & (RING - 1)];
                     yprev = y;
                     acc = __shfl_down_sync(0xffffffff, acc, 1);
-                    if (lane >= r - 1) acc = 0.0;
+                    if (lane >= LW) acc = 0.0;
                 }
             }
             asm volatile("cp.async.wait_group 0;" ::: "memory");
         } else {
             // ------------------------------------------------- producers
-            // Two register buffers alternate so the next row's factor loads are
-            // always in flight while the current row gathers and reduces.
             constexpr int NP = NW - 1;
+            // The lex-latest line of the producers' stencil in each earlier row of
+            // lines: once its value at the frontier x is visible, everything the
+            // row needs has almost certainly been produced (per-value sentinel
+            // checks remain the guard).
+            int dep1, dep2;
+            if (FWD) {
+                dep1 = (g.d > 1 && iy > 1) ? L - 2 : -1;
+                dep2 = (g.d > 2 && iz > 0) ? min(iy + r, K - 1) + K * (iz - 1) : -1;
+            } else {
+                dep1 = (g.d > 1 && iy < K - 2) ? L + 2 : -1;
+                dep2 = (g.d > 2 && iz < K - 1) ? max(iy - r, 0) + K * (iz + 1) : -1;
+            }
             double va[CH], vb[CH];
             double ra = 0.0, rb = 0.0;   // rhs of the row, loaded with its factors
-            auto load_v = [&](int t, double (&dst)[CH], int b0) {
+            auto load_v = [&](int t, double (&dst)[CH], double &rd, int b0) {
                 const int ix = FWD ? t : K - 1 - t;
                 const double *row = a.lu + (size_t)(row0 + ix) * g.S + a.lo;
-                if (b0 == 0 && t < K) (&dst == &va ? ra : rb) = a.rhs[row0 + ix];
+                if (b0 == 0 && t < K) rd = a.rhs[row0 + ix];
 #pragma unroll
                 for (int j = 0; j < CH; ++j) {
                     const int jj = b0 + lane + 32 * j;
@@ -294,32 +290,21 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
             auto process = [&](int t, double (&v)[CH], double rhs_i) {
                 const int ix = FWD ? t : K - 1 - t;
                 const int64_t i = row0 + ix;
-                double acc = 0.0;
-#ifdef LP_SWEEP_TRACE
-                int npoll = 0, lastjj = -1;
-                unsigned long long *rt = nullptr;
-                if (a.trace && (tl == g.nlines / 2 - 1 || tl == g.nlines / 2))
-                    rt = a.trace + (size_t)g.nlines * 4 + (size_t)(tl == g.nlines / 2 - 1 ? 0 : 1) * K * 6 + (size_t)t * 6;
-                if (rt && lane == 0) rt[0] = gtime();
-#endif
                 if (lane < 2) {
                     const int dl = lane == 0 ? dep1 : dep2;
                     if (dl >= 0) {
                         const int fx = FWD ? min(ix + r, K - 1) : max(ix - r, 0);
                         const double *fp = a.out + (int64_t)dl * K + fx;
-                        while (bits(ld_poll(fp)) == SWEEP_SENTINEL) LP_BACKOFF();
+                        while (bits(ld_poll(fp)) == SWEEP_SENTINEL) __nanosleep(LP_SWEEP_SLEEP);
                     }
                 }
                 __syncwarp();
-#ifdef LP_SWEEP_TRACE
-                if (rt && lane == 0) rt[4] = gtime();
-#endif
-#ifdef LP_SWEEP_SERIAL_ONLY
-                for (int b0 = 0; b0 < 0; b0 += 32 * CH) {
-#else
+                double acc = 0.0;
                 for (int b0 = 0; b0 < a.nslot; b0 += 32 * CH) {
-#endif
-                    if (b0 > 0) load_v(t, v, b0);
+                    if (b0 > 0) {
+                        double dummy;
+                        load_v(t, v, dummy, b0);
+                    }
                     double yv[CH];
 #pragma unroll
                     for (int j = 0; j < CH; ++j) {
@@ -330,76 +315,34 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                     }
 #pragma unroll
                     for (int j = 0; j < CH; ++j) {
-                        // values not yet produced by their (earlier) lines: re-poll
                         if (bits(yv[j]) == SWEEP_SENTINEL) {
                             const int jj = b0 + lane + 32 * j;
                             yv[j] = ld_poll(a.out + i + s_delta[jj]);
                             while (bits(yv[j]) == SWEEP_SENTINEL) {
-                                LP_BACKOFF();
+                                __nanosleep(LP_SWEEP_SLEEP);
                                 yv[j] = ld_poll(a.out + i + s_delta[jj]);
-#ifdef LP_SWEEP_TRACE
-                                ++npoll;
-                                lastjj = jj;
-#endif
                             }
                         }
                         acc = fma(v[j], yv[j], acc);
                     }
                 }
-#ifdef LP_SWEEP_TRACE
-                {
-                    unsigned long long tg = gtime();
-                    for (int o = 16; o; o >>= 1) {
-                        tg = max(tg, (unsigned long long)__shfl_xor_sync(0xffffffff, (long long)tg, o));
-                        npoll += __shfl_xor_sync(0xffffffff, npoll, o);
-                        lastjj = max(lastjj, __shfl_xor_sync(0xffffffff, lastjj, o));
-                    }
-                    if (rt && lane == 0) {
-                        rt[1] = tg;
-
-                    }
-                }
-#endif
+                __syncwarp();
                 acc = warp_sum(acc);
                 if (lane == 0) {
                     const int slot = t & (RING - 1);
                     const unsigned long long free_tag = bits(ring_sent(t));
-#ifdef LP_SWEEP_TRACE
-                    int ringspins = 0;
-#endif
-                    while (bits(v_c[slot]) != free_tag) {
-#ifdef LP_SWEEP_TRACE
-                        ++ringspins;
-#endif
-#ifndef LP_SWEEP_RINGSPIN
-                        LP_BACKOFF();
-#endif
-                    }
-#ifdef LP_SWEEP_TRACE
-                    if (rt) rt[5] = (unsigned long long)ringspins;
-#endif
-#ifdef LP_SWEEP_NORHS
-                    v_c[slot] = canon(-acc);
-#else
+                    while (bits(v_c[slot]) != free_tag) __nanosleep(LP_SWEEP_SLEEP);
                     v_c[slot] = canon(rhs_i - acc);
-#endif
-#ifdef LP_SWEEP_TRACE
-                    if (rt) rt[2] = gtime();
-#endif
                 }
             };
-            int t = warp < LP_SWEEP_SERIAL_WARP ? warp : warp - 1;
-            load_v(t, va, 0);
+            int t = warp;
+            load_v(t, va, ra, 0);
             while (t < K) {
-#ifndef LP_SWEEP_NOPREFETCH
-                load_v(t + NP, vb, 0);
-#endif
+                load_v(t + NP, vb, rb, 0);
                 process(t, va, ra);
                 t += NP;
                 if (t >= K) break;
-#ifndef LP_SWEEP_NOPREFETCH
-                load_v(t + NP, va, 0);
-#endif
+                load_v(t + NP, va, ra, 0);
                 process(t, vb, rb);
                 t += NP;
             }
@@ -407,22 +350,29 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
     }
 }
 
-__global__ void band_kernel(Geom g, const double *__restrict__ lu, double *__restrict__ blo,
-                            double *__restrict__ bup, double *__restrict__ dg) {
-    const int64_t total = g.n * g.r;
+// band[row] = [ in-line: M(row, row-1-q) or M(row, row+1+q), q < r |
+//               line -/+1: M(row, slot(ox, -/+1)), ox = -r..r | pad ],  rdiag = 1/U_tt
+__global__ void band_kernel(Geom g, const double *__restrict__ lu, int bs, double *__restrict__ blo,
+                            double *__restrict__ bup, double *__restrict__ rdg) {
+    const int64_t total = g.n * bs;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
          q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = q / g.r;
-        const int l = (int)(q % g.r);
+        const int64_t i = q / bs;
+        const int l = (int)(q % bs);
         const double *row = lu + (size_t)i * g.S;
-        blo[q] = row[g.c - 1 - l];
-        bup[q] = row[g.c + 1 + l];
-        if (l == 0) dg[i] = 1.0 / row[g.c];
+        double lo = 0.0, up = 0.0;
+        if (l < g.r) {
+            lo = row[g.c - 1 - l];
+            up = row[g.c + 1 + l];
+        } else if (g.d > 1 && l < 3 * g.r + 1) {
+            const int j = l - g.r;   // ox = j - r
+            lo = row[g.c - g.W - g.r + j];
+            up = row[g.c + g.W - g.r + j];
+        }
+        blo[q] = lo;
+        bup[q] = up;
+        if (l == 0) rdg[i] = 1.0 / row[g.c];
     }
-    if (g.r == 0)
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
-             i += (int64_t)gridDim.x * blockDim.x)
-            dg[i] = 1.0 / lu[(size_t)i * g.S + g.c];
 }
 
 __global__ void fill_sentinel(int64_t n, double *a, double *b) {
@@ -443,45 +393,7 @@ int prefill(int64_t n, double *a, double *b, cudaStream_t st) {
     return LP_OK;
 }
 
-template <bool FWD, int CH>
-int run_sweep(const SweepArgs &a, const Geom &g, size_t smem, cudaStream_t st);
-
-template <bool FWD>
-int launch_sweep(lp_ilu *m, const double *rhs, double *out, cudaStream_t st) {
-    Geom g = geom_of(m->box);
-    LP_ARG(g.r <= 30, "stencil reach %d > 30 is not supported by the sweep kernel", g.r);
-    SweepArgs a;
-    a.g = g;
-    a.lu = m->box.lu;
-    a.band = FWD ? m->box.band_lo : m->box.band_up;
-    a.diag = m->box.diag;
-    a.rhs = rhs;
-    a.out = out;
-    a.ticket = m->ticket + (FWD ? 0 : 1);
-    a.lo = FWD ? 0 : g.c + g.r + 1;
-    a.nslot = FWD ? g.c - g.r : g.S - (g.c + g.r + 1);
-    a.trace = nullptr;
-#ifdef LP_SWEEP_TRACE
-    {
-        static unsigned long long *tr = nullptr;
-        static size_t trn = 0;
-        if (trn < (size_t)g.nlines * 4 + (size_t)12 * g.K) {
-            if (tr) dfree(tr);
-            trn = (size_t)g.nlines * 4 + (size_t)12 * g.K;
-            dalloc(&tr, trn, "sweep trace");
-        }
-        cudaMemsetAsync(tr, 0, trn * 8, st);
-        a.trace = tr;
-        g_trace = tr;
-        g_trace_n = trn;
-    }
-#endif
-    const size_t smem = (size_t)a.nslot * (sizeof(int) + 4) + 16;
-    LP_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(int), st));
-    if (a.nslot <= 32 * 8) return run_sweep<FWD, 8>(a, g, smem, st);
-    if (a.nslot <= 32 * 13) return run_sweep<FWD, 13>(a, g, smem, st);
-    return run_sweep<FWD, 16>(a, g, smem, st);
-}
+int band_stride(const Geom &g) { return (int)round_up(3 * g.r + 1, 2); }
 
 template <bool FWD, int CH>
 int run_sweep(const SweepArgs &a, const Geom &g, size_t smem, cudaStream_t st) {
@@ -506,17 +418,59 @@ int run_sweep(const SweepArgs &a, const Geom &g, size_t smem, cudaStream_t st) {
     return LP_OK;
 }
 
+template <bool FWD>
+int launch_sweep(lp_ilu *m, const double *rhs, double *out, cudaStream_t st) {
+    Geom g = geom_of(m->box);
+    LP_ARG(g.r <= 15, "stencil reach %d > 15 is not supported by the sweep kernel", g.r);
+    SweepArgs a;
+    a.g = g;
+    a.lu = m->box.lu;
+    a.band = FWD ? m->box.band_lo : m->box.band_up;
+    a.rdiag = m->box.diag;
+    a.rhs = rhs;
+    a.out = out;
+    a.ticket = m->ticket + (FWD ? 0 : 1);
+    a.bs = band_stride(g);
+    // producers: everything except the in-line entries and (d >= 2) line -/+1
+    const int excl = g.d > 1 ? g.W + g.r : g.r;
+    a.lo = FWD ? 0 : g.c + excl + 1;
+    a.nslot = FWD ? g.c - excl : g.S - (g.c + excl + 1);
+    a.trace = nullptr;
+#ifdef LP_SWEEP_TRACE
+    {
+        static unsigned long long *tr = nullptr;
+        static size_t trn = 0;
+        if (trn < (size_t)g.nlines * 4) {
+            if (tr) dfree(tr);
+            trn = (size_t)g.nlines * 4;
+            dalloc(&tr, trn, "sweep trace");
+        }
+        cudaMemsetAsync(tr, 0, trn * 8, st);
+        a.trace = tr;
+        g_trace = tr;
+        g_trace_n = trn;
+    }
+#endif
+    const size_t smem = (size_t)BRING * a.bs * sizeof(double) + BRING * sizeof(double) +
+                        (size_t)a.nslot * (sizeof(int) + 4) + 16;
+    LP_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(int), st));
+    if (a.nslot <= 32 * 8) return run_sweep<FWD, 8>(a, g, smem, st);
+    if (a.nslot <= 32 * 13) return run_sweep<FWD, 13>(a, g, smem, st);
+    return run_sweep<FWD, 16>(a, g, smem, st);
+}
+
 }  // namespace
 
 int box_build_bands(lp_ilu *m, cudaStream_t st) {
     BoxLayout &b = m->box;
     Geom g = geom_of(b);
+    const int bs = band_stride(g);
     int rc;
-    if (!b.band_lo && ((rc = dalloc(&b.band_lo, (size_t)b.n * g.r, "band")) ||
-                       (rc = dalloc(&b.band_up, (size_t)b.n * g.r, "band")) ||
+    if (!b.band_lo && ((rc = dalloc(&b.band_lo, (size_t)b.n * bs, "band")) ||
+                       (rc = dalloc(&b.band_up, (size_t)b.n * bs, "band")) ||
                        (rc = dalloc(&b.diag, (size_t)b.n, "diag"))))
         return rc;
-    band_kernel<<<148 * 8, 256, 0, st>>>(g, b.lu, b.band_lo, b.band_up, b.diag);
+    band_kernel<<<148 * 8, 256, 0, st>>>(g, b.lu, bs, b.band_lo, b.band_up, b.diag);
     count_launch();
     LP_CHECK_LAUNCH();
     return LP_OK;

@@ -35,11 +35,3 @@ for L in list(range(0, 12)) + list(range(nl // 2, nl // 2 + 4)) + list(range(nl 
 d0 = np.diff(t[:, 1])
 print("lead (row0 to row0) median us", np.median(d0), "line duration median",
       np.median(t[:, 3] - t[:, 1]), "start->row0 median", np.median(t[:, 1] - t[:, 0]))
-buf2 = np.zeros(nl * 4 + 12 * w.K, dtype=np.uint64)
-lib.lp_debug_sweep_trace(buf2.ctypes.data_as(ctypes.c_void_p), ctypes.c_int64(buf2.size))
-rows = buf2[nl * 4:].reshape(2, w.K, 6).astype(np.int64)
-for which in (0, 1):
-    rr = (rows[which][:, :5] - t0) / 1e3
-    print("line", nl // 2 - 1 + which, "t: proc_start polled gathered written consumed | npolls")
-    for tt in list(range(0, 20)) + list(range(w.K // 2, w.K // 2 + 24)):
-        print(tt, *[f"{rr[tt][c]:9.2f}" for c in (0, 4, 1, 2, 3)], "|", rows[which][tt][5])
