@@ -237,7 +237,11 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                     // c_t from the producers, read one step ahead by all lanes
                     double cc = cn;
                     const unsigned long long sb = bits(ring_sent(t));
+#ifdef LP_EXP_NOWAIT
+                    if (false) {
+#else
                     if (bits(cc) == sb) {
+#endif
                         do {
                             cc = v_c[slot];
                         } while (bits(cc) == sb);
@@ -284,7 +288,11 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
 #pragma unroll
                 for (int j = 0; j < CH; ++j) {
                     const int jj = b0 + lane + 32 * j;
+#ifdef LP_EXP_NOPROD
+                    dst[j] = 0.0 * jj;
+#else
                     dst[j] = (t < K && jj < a.nslot) ? __ldcs(row + jj) : 0.0;
+#endif
                 }
             };
             auto process = [&](int t, double (&v)[CH], double rhs_i) {
@@ -300,7 +308,11 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                 }
                 __syncwarp();
                 double acc = 0.0;
+#ifdef LP_EXP_NOPROD
+                for (int b0 = 0; b0 < 0; b0 += 32 * CH) {
+#else
                 for (int b0 = 0; b0 < a.nslot; b0 += 32 * CH) {
+#endif
                     if (b0 > 0) {
                         double dummy;
                         load_v(t, v, dummy, b0);

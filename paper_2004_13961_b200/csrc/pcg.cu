@@ -23,14 +23,21 @@ enum { S_RR = 0, S_RHO0 = 2, S_RHO1 = 4, S_CURV = 6, S_FF = 8, S_NSLOTS = 10 };
 struct Workspace {
     double *r = nullptr, *z = nullptr, *p = nullptr, *w = nullptr;
     double *partial = nullptr, *scal = nullptr;
-    double *host = nullptr;   // pinned status block
     ~Workspace() {
         double *ps[] = {r, z, p, w, partial, scal};
         for (double *q : ps)
             if (q) dfree(q);
-        if (host) cudaFreeHost(host);
     }
 };
+
+// Pinned status block, allocated once per host thread: cudaMallocHost /
+// cudaFreeHost per solve cost milliseconds (and cudaFreeHost synchronises the
+// device).
+double *status_block() {
+    static thread_local double *blk = nullptr;
+    if (!blk && cudaMallocHost((void **)&blk, 4 * sizeof(double)) != cudaSuccess) blk = nullptr;
+    return blk;
+}
 
 }  // namespace
 
@@ -55,7 +62,8 @@ extern "C" int lp_pcg_solve(lp_operator *op, lp_ilu *pre, const double *F, doubl
         (rc = dalloc(&ws.scal, S_NSLOTS, "scalars")))
         return rc;
     if (pre && (rc = dalloc(&ws.z, n, "z"))) return rc;
-    LP_CUDA(cudaMallocHost((void **)&ws.host, 4 * sizeof(double)));
+    double *const host = status_block();
+    LP_ARG(host != nullptr, "cannot allocate the pinned status block");
     double *sc = ws.scal;
 
     // ||f|| and the initial residual
@@ -63,9 +71,9 @@ extern "C" int lp_pcg_solve(lp_operator *op, lp_ilu *pre, const double *F, doubl
     bool x_nonzero = false;
     if (has_x0) {
         if ((rc = dot_dd(n, x, x, ws.partial, sc + S_RR, st))) return rc;
-        LP_CUDA(cudaMemcpyAsync(ws.host, sc + S_RR, sizeof(double), cudaMemcpyDeviceToHost, st));
+        LP_CUDA(cudaMemcpyAsync(host, sc + S_RR, sizeof(double), cudaMemcpyDeviceToHost, st));
         LP_CUDA(cudaStreamSynchronize(st));
-        x_nonzero = ws.host[0] != 0.0;
+        x_nonzero = host[0] != 0.0;
     } else {
         LP_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), st));
     }
@@ -76,11 +84,11 @@ extern "C" int lp_pcg_solve(lp_operator *op, lp_ilu *pre, const double *F, doubl
         LP_CUDA(cudaMemcpyAsync(ws.r, F, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
     if ((rc = dot_dd(n, ws.r, ws.r, ws.partial, sc + S_RR, st))) return rc;
-    LP_CUDA(cudaMemcpyAsync(ws.host, sc + S_RR, sizeof(double), cudaMemcpyDeviceToHost, st));
-    LP_CUDA(cudaMemcpyAsync(ws.host + 2, sc + S_FF, sizeof(double), cudaMemcpyDeviceToHost, st));
+    LP_CUDA(cudaMemcpyAsync(host, sc + S_RR, sizeof(double), cudaMemcpyDeviceToHost, st));
+    LP_CUDA(cudaMemcpyAsync(host + 2, sc + S_FF, sizeof(double), cudaMemcpyDeviceToHost, st));
     LP_CUDA(cudaStreamSynchronize(st));
-    const double fnorm = sqrt(ws.host[2]);
-    double rr = ws.host[0];
+    const double fnorm = sqrt(host[2]);
+    double rr = host[0];
     if (history) history[0] = sqrt(rr);
 
     int64_t it = 0;
@@ -102,17 +110,17 @@ extern "C" int lp_pcg_solve(lp_operator *op, lp_ilu *pre, const double *F, doubl
         if ((rc = pcg_update_xr(n, x, ws.r, ws.p, ws.w, rho_new, sc + S_CURV, ws.partial, st)))
             return rc;
         if ((rc = finalize_dd(ws.partial, sc + S_RR, st))) return rc;
-        LP_CUDA(cudaMemcpyAsync(ws.host, sc + S_RR, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-        LP_CUDA(cudaMemcpyAsync(ws.host + 2, sc + S_CURV, sizeof(double), cudaMemcpyDeviceToHost, st));
+        LP_CUDA(cudaMemcpyAsync(host, sc + S_RR, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        LP_CUDA(cudaMemcpyAsync(host + 2, sc + S_CURV, sizeof(double), cudaMemcpyDeviceToHost, st));
         LP_CUDA(cudaStreamSynchronize(st));
-        const double curv = ws.host[2];
+        const double curv = host[2];
         if (curv <= 0.0) {
             rep->iterations = it;
             rep->indefinite_value = curv;
             set_error("non-positive curvature p'Ap = %.3e at iteration %lld", curv, (long long)it);
             return LP_ERR_INDEFINITE;
         }
-        rr = ws.host[0];
+        rr = host[0];
         if (history) history[it] = sqrt(rr);
     }
     const auto t1 = std::chrono::steady_clock::now();
