@@ -36,6 +36,7 @@
 namespace lp {
 
 unsigned long long *g_trace = nullptr;   // LP_SWEEP_TRACE builds only
+__device__ long long g_chk[8];            // LP_SWEEP_CHECK builds: first failed check
 size_t g_trace_n = 0;
 
 constexpr unsigned long long SWEEP_SENTINEL = 0xFFF4C0FFEE5EED00ull;   // signalling NaN
@@ -44,6 +45,8 @@ namespace {
 
 constexpr int RING = 64;    // rows in flight per line (power of two)
 constexpr int BRING = 128;  // band rows staged for the serial warp (power of two)
+constexpr int PR = 8;       // rows per producer stage (2-D)
+constexpr int NSTAGE = 5;   // producer stages in flight (2-D)
 constexpr unsigned long long RING_SENT = 0xFFF5000000000000ull;
 
 #ifndef LP_SWEEP_SLEEP
@@ -64,6 +67,31 @@ __device__ __forceinline__ double ld_poll(const double *p) {
     double v;
     asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
     return v;
+}
+
+// Shared-memory accesses through 32-bit shared-window addresses (computed once;
+// generic pointers make the compiler re-derive the window base every step).
+__device__ __forceinline__ unsigned smem_addr(const void *p) {
+    unsigned a;
+    // opaque to the compiler, so the value stays in a register
+    asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(a) : "l"(p));
+    return a;
+}
+__device__ __forceinline__ double lds(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void lds2(unsigned a, double &x, double &y) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+__device__ __forceinline__ double lds_v(unsigned a) {
+    double v;
+    asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_v(unsigned a, double v) {
+    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 
 __device__ __forceinline__ double ring_sent(int t) {
@@ -89,13 +117,16 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
 struct SweepArgs {
     Geom g;
     const double *lu;     // factors [n][S]
-    const double *band;   // [n][bs]: r in-line coefficients, then the 2r+1 of line L-/+1
-    const double *rdiag;  // 1/U_tt
+    const double *band;   // [n][NQ]: in-line coefficients (see band_kernel)
     const double *rhs;
     double *out;
     int *ticket;
-    int bs;               // band row stride (even)
+    const double *band_g; // [n][gsz]: line L-/+1 coefficients (band + n * NQ)
+    int gsz;              // their padded size (even)
     int lo, nslot;        // producers' slot range [lo, lo + nslot)
+    int pr_rs, pr_ww;     // 2-D staged producers: factor row stride / y-window width (doubles)
+    unsigned pr_ofs;      // byte offset of the producers' staging region in dynamic smem
+    int nseg;             // 2-D: lines of the producers' stencil (r - 1)
     unsigned long long *trace;   // LP_SWEEP_TRACE builds: per-line timestamps
 };
 
@@ -105,25 +136,91 @@ __device__ __forceinline__ unsigned long long gtime() {
     return t;
 }
 
-template <bool FWD, int NW, int CH>
+__device__ __forceinline__ void mbar_init(unsigned a, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned a, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned bytes, unsigned mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
+    asm volatile("{\n .reg .pred p;\n LP_W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 " @!p bra LP_W%=;\n}" ::"r"(a), "r"(parity) : "memory");
+}
+
+// One TMA bulk copy (two at the ring wrap) of the w-double rows of steps
+// [32c, 32c + 32) of a line into a BRING-row shared ring (ring row = ix mod BRING),
+// completing on mbarrier `mbar` (slot c mod 4).  Issued by one lane.
+template <bool FWD>
+__device__ __forceinline__ void stage_chunk(const double *src, int w, unsigned ring, int64_t row0,
+                                            int K, int c, unsigned mbar) {
+    const int u0 = 32 * c;
+    if (u0 >= K) return;
+    const int u1 = min(u0 + 32, K);
+    const int ixlo = FWD ? u0 : K - u1, ixhi = FWD ? u1 : K - u0;
+    const unsigned rb = (unsigned)w * 8;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect(mbar, (unsigned)(ixhi - ixlo) * rb);
+    int p0 = ixlo;
+    while (p0 < ixhi) {
+        const int p1 = min(ixhi, (p0 / BRING + 1) * BRING);
+        bulk_g2s(ring + (unsigned)(p0 & (BRING - 1)) * rb, src + (size_t)(row0 + p0) * w,
+                 (unsigned)(p1 - p0) * rb, mbar);
+        p0 = p1;
+    }
+}
+
+// Warp roles: warps with id mod 4 in {0, 1} produce c_t = rhs_t - (stencil part
+// in lines L-/+2 and older / other planes); warp NW-2 ("group") adds the 2r+1 entries of line
+// L-/+1 as their values arrive and hands d_t = c_t - A_t to warp NW-1
+// ("serial"), which runs the in-line recurrence y_t = d_t - sum_q l_q y_{t-q}
+// entirely in registers (every lane redundantly; no shuffles on the chain).
+template <bool FWD, int NW, int CH, int NQ>
 __global__ void __launch_bounds__(32 * NW)
 box_sweep_kernel(const __grid_constant__ SweepArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const Geom &g = a.g;
-    double *s_band = reinterpret_cast<double *>(dsm);                  // [BRING][bs]
-    double *s_rd = s_band + (size_t)BRING * a.bs;                       // [BRING]
-    int *s_delta = reinterpret_cast<int *>(s_rd + BRING);               // [nslot]
+    double *s_in = reinterpret_cast<double *>(dsm);                     // [BRING][NQ]
+    double *s_grp = s_in + (size_t)BRING * NQ;                          // [BRING][gsz]
+    int *s_delta = reinterpret_cast<int *>(s_grp + (size_t)BRING * a.gsz);   // [nslot]
     signed char *s_ox = reinterpret_cast<signed char *>(s_delta + a.nslot);
     signed char *s_oy = s_ox + a.nslot;
     signed char *s_oz = s_oy + a.nslot;
     unsigned char *s_ok = reinterpret_cast<unsigned char *>(s_oz + a.nslot);
-    __shared__ double s_c[RING];
+    __shared__ __align__(8) unsigned long long s_mbar[8];   // chunk barriers: serial 0-3, group 4-7
+    __shared__ __align__(8) unsigned long long s_pfull[NSTAGE];
+    // stages consumed per ring slot (a counter, not an mbarrier: a loader can be
+    // two phases ahead of a slow consumer, where a parity wait would alias)
+    __shared__ unsigned s_pcons[NSTAGE];
+    __shared__ double s_c[RING];   // producers -> serial: c_t
+    __shared__ double s_d[RING];   // group -> serial: A_t (line L-/+1 part)
     __shared__ int s_line;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int K = g.K, r = g.r;
     volatile double *v_c = s_c;
-    constexpr int SERIAL = NW - 1;   // highest warp id: favoured by the SMSP arbiter
+    volatile double *v_d = s_d;
+    constexpr int SERIAL = NW - 1;   // highest warp ids: favoured by the SMSP arbiter
+    constexpr int GROUP = NW - 2;
 
+    if (tid == 0) {
+        for (int i = 0; i < 8; ++i) mbar_init(smem_addr(s_mbar + i), 1);
+        for (int i = 0; i < NSTAGE; ++i) {
+            mbar_init(smem_addr(s_pfull + i), 1);
+            s_pcons[i] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    unsigned chunk_base = 0;   // chunks this warp has staged on earlier lines (mbarrier phases)
+    unsigned stage_base = 0;   // producer stages of earlier lines (2-D; mbarrier phases)
+    int *s_yofs = reinterpret_cast<int *>(dsm + a.pr_ofs + (size_t)NSTAGE * (PR * a.pr_rs + a.nseg * a.pr_ww) * 8);
+    if (g.d == 2)
+        for (int j = tid; j < a.nslot; j += blockDim.x) s_yofs[j] = (j / g.W) * a.pr_ww + j % g.W;
     for (int j = tid; j < a.nslot; j += blockDim.x) {
         int sx, sy, sz;
         slot_axes(g, a.lo + j, sx, sy, sz);
@@ -136,7 +233,10 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
     for (;;) {
         __syncthreads();
         if (tid == 0) s_line = atomicAdd(a.ticket, 1);
-        for (int k = tid; k < RING; k += blockDim.x) s_c[k] = ring_sent(k);
+        for (int k = tid; k < RING; k += blockDim.x) {
+            s_c[k] = ring_sent(k);
+            s_d[k] = ring_sent(k);
+        }
         __syncthreads();
         const int tl = s_line;
         if (tl >= g.nlines) return;
@@ -148,125 +248,400 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
         }
         const int64_t row0 = (int64_t)L * K;
 #ifdef LP_SWEEP_TRACE
-        if (tid == 0 && a.trace) a.trace[(size_t)tl * 4] = gtime();
+        if (tid == 0 && a.trace) a.trace[(size_t)tl * 16] = gtime();
 #endif
         __syncthreads();
+        auto ix_of = [&](int t) { return FWD ? t : K - 1 - t; };
 
         if (warp == SERIAL) {
             // ------------------------------------------- serial recurrence
+            // Lane k owns the rows t == k (mod 32): sp = its row's in-line sum over
+            // the steps q >= 2, accumulated as those values are produced (one FMA
+            // per lane per step).  Row t+1's finished sum is broadcast during step
+            // t, off the chain; every lane then forms the same
+            //   y_t = fma(-e_1(t-1), y_{t-1}, rd_t d_t - sp_t).
+            // All addresses advance incrementally (the warp is latency bound: a
+            // step is a few dozen dependent-issue instructions).
+            constexpr unsigned RB = BRING * NQ * 8;        // ring bytes (power of two)
+            const unsigned in0 = smem_addr(s_in), d0 = smem_addr(s_d), c0 = smem_addr(s_c);
+            const unsigned mb = smem_addr(s_mbar);
             const bool has_prev = g.d > 1 && (FWD ? iy > 0 : iy < K - 1);
-            const double *prev = a.out + (FWD ? row0 - K : row0 + K);   // line L-/+1
-            const int LW = g.d > 1 ? 2 * r : r - 1;   // lanes >= LW hold no pending sum
-            auto ix_of = [&](int t) { return FWD ? t : K - 1 - t; };
-            // band rows of steps [u0, u0+32), contiguous in memory, by ix mod BRING
-            auto stage_chunk = [&](int u0) {
-                if (u0 < K) {
-                    const int u1 = min(u0 + 32, K);
-                    const int ixlo = FWD ? u0 : K - u1, ixhi = FWD ? u1 : K - u0;
-                    for (int p0 = ixlo; p0 < ixhi;) {
-                        const int p1 = min(ixhi, (p0 / BRING + 1) * BRING);
-                        const double *src = a.band + (size_t)(row0 + p0) * a.bs;
-                        double *dst = s_band + (size_t)(p0 & (BRING - 1)) * a.bs;
-                        const int n = (p1 - p0) * a.bs;
-                        for (int e = 2 * lane; e < n; e += 64) cp_async16(dst + e, src + e);
-                        if (!FWD)
-                            for (int e = lane; e < p1 - p0; e += 32)
-                                cp_async8(s_rd + ((p0 + e) & (BRING - 1)), a.rdiag + row0 + p0 + e);
-                        p0 = p1;
-                    }
-                }
-                asm volatile("cp.async.commit_group;" ::: "memory");
+            const int nch = (K + 31) / 32;
+            auto stage = [&](int c) {   // chunk c of this line (steps [32c, 32c+32))
+                if (lane == 0 && c < nch)
+                    stage_chunk<FWD>(a.band, NQ, in0, row0, K, c, mb + 8 * ((chunk_base + c) & 3));
             };
-            // lane k's two coefficients for step t (row t+k):
-            //   qi: in-line, multiplies y_{t-1} (lane 0: l1_t)
-            //   qg: line L-/+1, multiplies the step's new value y(L-/+1, t -/+ r)
-            auto coefs = [&](int t, double &qi, double &qg) {
-                const int tk = t + lane;
-                qi = 0.0;
-                qg = 0.0;
-                if (tk < 0 || tk >= K) return;
-                const double *b = s_band + (size_t)(ix_of(tk) & (BRING - 1)) * a.bs;
-                if (lane < r) qi = b[lane];
-                if (g.d > 1 && lane <= 2 * r) qg = b[r + (FWD ? 2 * r - lane : lane)];
-            };
-            auto xnew_of = [&](int t) { return FWD ? t + r : K - 1 - t - r; };
-            auto fetch_new = [&](int t) -> double {
-                const int x = xnew_of(t);
-                return (has_prev && x >= 0 && x < K) ? ld_poll(prev + x) : 0.0;
-            };
-            auto ready_new = [&](int t, double v) -> double {
-                const int x = xnew_of(t);
-                if (!has_prev || x < 0 || x >= K) return 0.0;
-                while (bits(v) == SWEEP_SENTINEL) v = ld_poll(prev + x);
-                return v;
-            };
-
-            stage_chunk(0);
-            stage_chunk(32);
-            stage_chunk(64);
-            asm volatile("cp.async.wait_group 2;" ::: "memory");
-            __syncwarp();
-            double acc = 0.0, yprev = 0.0;
-            double ynext = fetch_new(g.d > 1 ? -r : 0);
-            // virtual steps t = -r..-1: values of line L-/+1 at x < r (x > K-1-r)
-            if (g.d > 1)
-                for (int t = -r; t < 0; ++t) {
-                    double qi, qg;
-                    coefs(t, qi, qg);
-                    const double yn = ready_new(t, ynext);
-                    ynext = fetch_new(t + 1);
-                    acc = fma(qg, yn, acc);
-                    acc = __shfl_down_sync(0xffffffff, acc, 1);
-                    if (lane >= LW) acc = 0.0;
-                }
-            double cn = v_c[0];
-            for (int t0 = 0; t0 < K; t0 += 32) {
-                stage_chunk(t0 + 96);
-                asm volatile("cp.async.wait_group 2;" ::: "memory");
-                __syncwarp();
-                const int tend = min(t0 + 32, K);
-                for (int t = t0; t < tend; ++t) {
-                    const int slot = t & (RING - 1);
-                    double qi, qg;
-                    coefs(t, qi, qg);
-                    const double yn = ready_new(t, ynext);
-                    ynext = fetch_new(t + 1);
-                    const double yb = __shfl_sync(0xffffffff, yprev, 0);
-                    acc = fma(qg, yn, acc);
-                    if (lane != 0) acc = fma(qi, yb, acc);
-                    // c_t from the producers, read one step ahead by all lanes
-                    double cc = cn;
-                    const unsigned long long sb = bits(ring_sent(t));
-#ifdef LP_EXP_NOWAIT
-                    if (false) {
-#else
-                    if (bits(cc) == sb) {
+#ifdef LP_SWEEP_TRACE
+            long long wcyc = 0;
 #endif
-                        do {
-                            cc = v_c[slot];
-                        } while (bits(cc) == sb);
+            auto wait_chunk = [&](int c) {
+#ifdef LP_SWEEP_TRACE
+                const long long w0 = clock64();
+#endif
+                if (c < nch) mbar_wait(mb + 8 * ((chunk_base + c) & 3), ((chunk_base + c) >> 2) & 1);
+#ifdef LP_SWEEP_TRACE
+                wcyc += clock64() - w0;
+#endif
+            };
+            stage(0);
+            stage(1);
+            stage(2);
+            wait_chunk(0);
+            unsigned roff = FWD ? 0u : (unsigned)(((K - 1) & (BRING - 1)) * NQ * 8);
+            const unsigned rstep = FWD ? NQ * 8u : (unsigned)(RB - NQ * 8);
+            unsigned doff = 0;
+            unsigned jl = (unsigned)lane;                   // (lane - t) & 31
+            double sp = 0.0, yprev = 0.0, e1 = 0.0;
+            double e1n, rdn;
+            lds2(in0 + roff, e1n, rdn);
+            double qn = (jl >= 2 && jl < NQ) ? lds(in0 + roff + 8 * jl) : 0.0;
+            double spn = 0.0;
+            double dn = has_prev ? lds_v(d0) : 0.0, cn = lds_v(c0);
+            double *outp = a.out + row0 + (FWD ? 0 : K - 1);
+            const ptrdiff_t ostep = FWD ? 1 : -1;
+            // loop bounds in registers (a "memory" clobber would otherwise make the
+            // compiler re-read them from the parameter bank every step)
+            int Kr;
+            asm volatile("mov.b32 %0, %1;" : "=r"(Kr) : "r"(K));
+            unsigned qoff = 8u * (unsigned)lane;   // 8 * ((lane - t) & 31)
+#ifdef LP_SWEEP_TRACE
+            long long nspin_c = 0, nspin_a = 0;
+#endif
+            auto step = [&](const int t) {
+                const double q = qn, e1c = e1n, rd = rdn, spt = spn;
+                double c = cn, av = dn;
+#ifdef LP_EXP_ALONE
+                c = 1.0;
+                av = 0.0;
+#else
+                const unsigned long long sb = bits(ring_sent(t));
+#ifdef LP_SWEEP_TRACE
+                while (bits(c) == sb) { c = lds_v(c0 + doff); ++nspin_c; }
+                if (has_prev)
+                    while (bits(av) == sb) { av = lds_v(d0 + doff); ++nspin_a; }
+#else
+                while (bits(c) == sb) c = lds_v(c0 + doff);
+                if (has_prev)
+                    while (bits(av) == sb) av = lds_v(d0 + doff);
+#endif
+#endif
+                const double y = fma(-e1, yprev, fma(rd, c - av, -spt));
+                // every lane stores the same values (no divergent branch)
+                sts_v(c0 + doff, ring_sent(t + RING));
+                if (has_prev) sts_v(d0 + doff, ring_sent(t + RING));
+#ifdef LP_EXP_NOSTORE
+                if (t == Kr - 1)
+#endif
+                __stcg(outp, canon(y));
+                outp += ostep;
+                doff = (doff + 8) & (RING * 8 - 1);
+                cn = lds_v(c0 + doff);
+                if (has_prev) dn = lds_v(d0 + doff);
+                roff = (roff + rstep) & (RB - 1);
+                qoff = (qoff - 8) & 255;
+                const unsigned rowa = in0 + roff;
+                lds2(rowa, e1n, rdn);
+                qn = (qoff - 16 < (NQ - 2) * 8) ? lds(rowa + qoff) : 0.0;
+                sp = ((unsigned)lane == ((unsigned)t & 31)) ? 0.0 : fma(q, y, sp);
+                // broadcast row t+1's finished sum (lane t+1 took no update this step)
+                spn = __shfl_sync(0xffffffff, sp, (t + 1) & 31);
+                e1 = e1c;
+                yprev = y;
+            };
+#ifdef LP_SWEEP_TRACE
+            auto mark = [&](int k) {
+                if (lane == 0 && a.trace) {
+                    a.trace[(size_t)tl * 16 + k] = gtime();
+                    a.trace[(size_t)tl * 16 + 4 + k] = clock64();
+                }
+            };
+            mark(1);
+#endif
+            for (int c = 0; c < nch; ++c) {
+                // chunk c+1 must be resident before step 32c+31 prefetches its first row
+                stage(c + 3);
+                wait_chunk(c + 1);
+                const int t1 = min(32 * c + 32, Kr);
+#ifdef LP_SWEEP_TRACE
+                const int th = Kr / 2;
+                if (32 * c <= th && th < t1) {
+                    for (int t = 32 * c; t < th; ++t) step(t);
+                    mark(2);
+                    for (int t = th; t < t1; ++t) step(t);
+                    continue;
+                }
+#endif
+                for (int t = 32 * c; t < t1; ++t) step(t);
+            }
+#ifdef LP_SWEEP_TRACE
+            mark(3);
+#endif
+#ifdef LP_SWEEP_TRACE
+            if (lane == 0 && a.trace) {
+                a.trace[(size_t)tl * 16 + 4] = wcyc;
+                a.trace[(size_t)tl * 16 + 13] = nspin_c;
+                a.trace[(size_t)tl * 16 + 14] = nspin_a;
+            }
+#endif
+            chunk_base += nch;
+        } else if (warp == GROUP) {
+#ifdef LP_EXP_ALONE
+            continue;
+#endif
+            // ------------------- line L-/+1 group: A_t (the serial forms c_t - A_t)
+            // Lane k owns the rows t == k (mod 32) and accumulates their 2r+1
+            // products with line L-/+1 as its values arrive (no shuffles on the
+            // sums).  The value y(L-/+1, x) arriving at step t = x -/+ r enters rows
+            // t..t+2r with the coefficients of band row x's group section.  Values
+            // are polled 32 at a time (one per lane) and the window is re-polled
+            // while the value needed next is not yet produced.
+            const bool has_prev = g.d > 1 && (FWD ? iy > 0 : iy < K - 1);
+            if (!has_prev) continue;
+            const double *prev = a.out + (FWD ? row0 - K : row0 + K);   // line L-/+1
+            const int R = r;
+            const unsigned gstride = (unsigned)a.gsz * 8;
+            const unsigned grp0 = smem_addr(s_grp), c0 = smem_addr(s_c), d0 = smem_addr(s_d);
+            const unsigned mb = smem_addr(s_mbar + 4);
+            const int nch = has_prev ? (K + 31) / 32 : 0;
+            // chunk c = arrival indices [32c, 32c+32): x = 32c.. (fwd) / K-1-32c.. (bwd)
+            auto stage = [&](int c) {
+                if (lane == 0 && c < nch)
+                    stage_chunk<FWD>(a.band_g, a.gsz, grp0, row0, K, c, mb + 8 * ((chunk_base + c) & 3));
+            };
+            auto wait_chunk = [&](int c) {
+                if (c < nch) mbar_wait(mb + 8 * ((chunk_base + c) & 3), ((chunk_base + c) >> 2) & 1);
+            };
+            stage(0);
+            stage(1);
+            stage(2);
+            wait_chunk(0);
+            const int tw = 2 * R;
+            double acc = 0.0;
+            double yb = 0.0;   // lane l: y(L-/+1, arrival index (uarr & ~31) + l)
+            double ybn = 0.0;  // the next block's values, polled half a block early
+            auto poll_block = [&](int u0) -> double {
+                const int ua = u0 + lane;
+                return (has_prev && ua < K) ? ld_poll(prev + (FWD ? ua : K - 1 - ua)) : 0.0;
+            };
+            // coefficient of arrival u for this lane's row (band row x(u), j = row - (u - R))
+            auto coef = [&](int u) -> double {
+                const int x = FWD ? u : K - 1 - u;
+                const int j = (lane - (u - R)) & 31;
+                return (u < K && j <= tw) ? lds(grp0 + (x & (BRING - 1)) * gstride + 8 * j) : 0.0;
+            };
+            int Kr;
+            asm volatile("mov.b32 %0, %1;" : "=r"(Kr) : "r"(K));
+            if (has_prev) ybn = poll_block(0);
+            double qn = 0.0, ynx = 0.0;   // the current step's coefficient and value
+#ifdef LP_SWEEP_TRACE
+            const long long gc0 = clock64();
+            long long nrepoll = 0;
+#endif
+            for (int t = -R; t < Kr; ++t) {
+                const int uarr = t + R;   // arrival index
+                const int t32 = uarr & 31;
+                if (t32 == 0) {
+                    stage((uarr >> 5) + 3);
+                    wait_chunk((uarr >> 5) + 1);
+                    yb = ybn;
+                    // the serial has consumed every slot this block will write
+                    if (t >= 0) {
+                        const int tl31 = t + 31;
+                        const unsigned long long fb = bits(ring_sent(tl31));
+                        while (bits(lds_v(d0 + (tl31 & (RING - 1)) * 8)) != fb) {
+                        }
                     }
-                    double y = fma(-qi, yprev, cc - acc);
-                    if (!FWD) y *= s_rd[ix_of(t) & (BRING - 1)];
-                    y = canon(y);
-                    if (lane == 0) {
-                        v_c[slot] = ring_sent(t + RING);
-                        __stcg(a.out + row0 + ix_of(t), y);
+                    __syncwarp();
+                    if (has_prev) {
+                        ynx = __shfl_sync(0xffffffff, yb, 0);
+                        qn = coef(uarr);
+                    }
+                } else if (t32 == 16 && has_prev) {
+                    ybn = poll_block(uarr + 16);
+                }
+                if (has_prev && uarr < Kr) {
+                    double yn = ynx;
+                    while (bits(yn) == SWEEP_SENTINEL) {
+                        // re-poll the rest of the window: one round trip brings in
+                        // every value produced since the last poll
+                        const int ua = uarr - t32 + lane;
+                        if (lane >= t32 && ua < Kr) yb = ld_poll(prev + (FWD ? ua : Kr - 1 - ua));
+                        yn = __shfl_sync(0xffffffff, yb, t32);
+#ifdef LP_SWEEP_TRACE
+                        ++nrepoll;
+#endif
                     }
 #ifdef LP_SWEEP_TRACE
-                    if (lane == 0 && a.trace && (t == 0 || t == K / 2 || t == K - 1))
-                        a.trace[(size_t)tl * 4 + (t == 0 ? 1 : (t == K - 1 ? 3 : 2))] = gtime();
+                    if (lane == 0 && a.trace && t == K / 2) a.trace[(size_t)tl * 16 + 10] = gtime();
 #endif
-                    cn = v_c[(t + 1) & (RING - 1)];
-                    yprev = y;
-                    acc = __shfl_down_sync(0xffffffff, acc, 1);
-                    if (lane >= LW) acc = 0.0;
+                    acc = fma(qn, yn, acc);
+                    if (t32 < 31) {   // next step's operands, off this step's path
+                        ynx = __shfl_sync(0xffffffff, yb, t32 + 1);
+                        qn = coef(uarr + 1);
+                    }
+                }
+                if (t >= 0 && lane == (t & 31)) {
+                    sts_v(d0 + (unsigned)(t & (RING - 1)) * 8, acc);
+                    acc = 0.0;
+                }
+                if (t >= 0) {
+#ifdef LP_SWEEP_TRACE
+                    if (lane == 0 && a.trace && t == K / 2) a.trace[(size_t)tl * 16 + 9] = gtime();
+#endif
                 }
             }
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
+#ifdef LP_SWEEP_TRACE
+            if (lane == 0 && a.trace) {
+                a.trace[(size_t)tl * 16 + 11] = clock64() - gc0;
+                a.trace[(size_t)tl * 16 + 12] = nrepoll;
+            }
+#endif
+            chunk_base += nch;
+        } else if ((warp & 3) >= 2) {
+            // keeps SMSPs 2 and 3 (warp id mod 4) to the group and serial warps:
+            // both are latency bound, and any co-scheduled busy warp steals their
+            // issue slots
+            continue;
         } else {
-            // ------------------------------------------------- producers
-            constexpr int NP = NW - 1;
+#ifdef LP_EXP_ALONE
+            continue;
+#endif
+            constexpr int NP = NW / 2;   // warps 0, 1, 4, 5, ... (SMSPs 0 and 1)
+            const int pw = (warp >> 2) * 2 + (warp & 1);
+#ifdef LP_EXP_OLDPROD
+            if (false) {
+#else
+            if (g.d == 2) {
+#endif
+                // ---- staged producers (2-D).  Stage s = PR consecutive rows (steps
+                // [PR s, PR s + PR)), taken by warp s mod NP.  Their factor rows arrive
+                // by TMA bulk copies into a NSTAGE-slot ring (full/empty mbarriers);
+                // the y values of lines L-/+2 .. L-/+r over the stage's x window are
+                // loaded once per stage into shared memory (sentinel-checked), and each
+                // row's dot product is then formed from shared memory only.
+                const int ns = (K + PR - 1) / PR;
+                const unsigned fb0 = smem_addr(dsm + a.pr_ofs);
+                const unsigned fslot = (unsigned)(PR * a.pr_rs) * 8;
+                const unsigned yb0 = fb0 + NSTAGE * fslot;
+                const unsigned yslot = (unsigned)(a.nseg * a.pr_ww) * 8;
+                const unsigned full0 = smem_addr(s_pfull);
+                volatile unsigned *v_cons = s_pcons;
+                const int W = g.W, nslot = a.nslot, ww = a.pr_ww;
+                const int oy0 = FWD ? -r : 2;   // line offset of segment 0
+                const int depL = FWD ? (iy >= 2 ? L - 2 : -1) : (iy <= K - 3 ? L + 2 : -1);
+                for (int st = pw; st < ns; st += NP) {
+                    const unsigned gs = stage_base + st;
+                    const unsigned slot = gs % NSTAGE;
+                    const int t0 = PR * st, t1 = min(t0 + PR, K), nr = t1 - t0;
+                    const int ixlo = FWD ? t0 : K - t1, ixhi = FWD ? t1 : K - t0;
+                    const unsigned fb = fb0 + slot * fslot, yb = yb0 + slot * yslot;
+                    // slot free: stage gs - NSTAGE (the previous user) consumed
+                    while (v_cons[slot] < gs / NSTAGE) {
+                    }
+                    // factor rows: one 16-byte aligned bulk copy per row
+                    if (lane == 0) {
+                        unsigned bytes = 0;
+                        for (int q = 0; q < nr; ++q) {
+                            const int64_t gi = (row0 + (FWD ? t0 + q : K - 1 - t0 - q)) * (int64_t)g.S + a.lo;
+                            bytes += (unsigned)((nslot + (int)(gi & 1) + 1) & ~1) * 8;
+                        }
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        mbar_expect(full0 + 8 * slot, bytes);
+                    }
+                    __syncwarp();
+                    double rhs_t = 0.0;
+                    int sh = 0;
+                    if (lane < nr) {
+                        const int ix = FWD ? t0 + lane : K - 1 - t0 - lane;
+                        const int64_t gi = (row0 + ix) * (int64_t)g.S + a.lo;
+                        sh = (int)(gi & 1);
+#ifdef LP_SWEEP_CHECK
+                        if (gi - sh < 0 || gi - sh + ((nslot + sh + 1) & ~1) > g.n * (int64_t)g.S + 2 || ix < 0 ||
+                            ix >= K || (fb - fb0) >= NSTAGE * fslot || ((fb + (unsigned)(lane * a.pr_rs) * 8) & 15)) {
+                            if (atomicCAS((unsigned long long *)g_chk, 0ull, 1ull) == 0ull) {
+                                g_chk[1] = L; g_chk[2] = st; g_chk[3] = lane; g_chk[4] = ix; g_chk[5] = gi;
+                                g_chk[6] = sh; g_chk[7] = fb - fb0;
+                            }
+                            asm volatile("exit;");
+                        }
+#endif
+                        bulk_g2s(fb + (unsigned)(lane * a.pr_rs) * 8, a.lu + (gi - sh),
+                                 (unsigned)((nslot + sh + 1) & ~1) * 8, full0 + 8 * slot);
+                        rhs_t = a.rhs[row0 + ix];
+                    }
+                    // y window of each stencil line: x in [ixlo - r, ixlo - r + ww)
+                    if (depL >= 0) {
+                        const int fx = FWD ? min(ixhi - 1 + r, K - 1) : max(ixlo - r, 0);
+                        const double *fp = a.out + (int64_t)depL * K + fx;
+                        while (bits(ld_poll(fp)) == SWEEP_SENTINEL) __nanosleep(LP_SWEEP_SLEEP);
+                    }
+                    for (int e = lane; e < a.nseg * ww; e += 32) {
+                        const int k = e / ww, w = e - k * ww;
+                        const int ly = iy + oy0 + k, x = ixlo - r + w;
+                        double v = 0.0;
+                        if (ly >= 0 && ly < K && x >= 0 && x < K) {
+                            const double *yp = a.out + (int64_t)ly * K + x;
+#ifdef LP_SWEEP_CHECK
+                            if (yp < a.out || yp >= a.out + g.n || 8 * e >= yslot) {
+                                if (atomicCAS((unsigned long long *)g_chk, 0ull, 2ull) == 0ull) {
+                                    g_chk[1] = L; g_chk[2] = st; g_chk[3] = e; g_chk[4] = ly; g_chk[5] = x;
+                                }
+                                asm volatile("exit;");
+                            }
+#endif
+                            v = __ldcg(yp);
+                            while (bits(v) == SWEEP_SENTINEL) {
+                                __nanosleep(LP_SWEEP_SLEEP);
+                                v = ld_poll(yp);
+                            }
+                        }
+                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(yb + 8 * e), "d"(v) : "memory");
+                    }
+                    __syncwarp();
+                    mbar_wait(full0 + 8 * slot, (gs / NSTAGE) & 1);
+                    // lane = (row q, part p): row q = lane & 7, slots p, p+4, ...
+                    const int q = lane & 7, part = lane >> 3;
+                    const int shq = __shfl_sync(0xffffffff, sh, q);
+                    double acc = 0.0;
+                    if (q < nr) {
+                        const int ixq = FWD ? t0 + q : K - 1 - t0 - q;
+                        const unsigned frow = fb + (unsigned)(q * a.pr_rs + shq) * 8;
+                        const unsigned yrow = yb + (unsigned)(ixq - ixlo) * 8;
+                        for (int j = part; j < nslot; j += 4) {
+#ifdef LP_SWEEP_CHECK
+                            if (frow + 8 * j >= fb0 + NSTAGE * fslot || yrow + 8 * s_yofs[j] >= yb + yslot ||
+                                yrow < yb) {
+                                if (atomicCAS((unsigned long long *)g_chk, 0ull, 3ull) == 0ull) {
+                                    g_chk[1] = L; g_chk[2] = st; g_chk[3] = q; g_chk[4] = j; g_chk[5] = s_yofs[j];
+                                    g_chk[6] = ixq; g_chk[7] = ixlo;
+                                }
+                                asm volatile("exit;");
+                            }
+#endif
+                            acc = fma(lds(frow + 8 * j), lds(yrow + 8 * s_yofs[j]), acc);
+                        }
+                    }
+                    acc += __shfl_xor_sync(0xffffffff, acc, 8);
+                    acc += __shfl_xor_sync(0xffffffff, acc, 16);
+                    __syncwarp();
+                    if (lane == 0) v_cons[slot] = gs / NSTAGE + 1;
+                    // hand c_t to the group (slots are freed in order: check the last)
+                    const int tl1 = t1 - 1;
+                    const unsigned long long free_tag = bits(ring_sent(tl1));
+                    if (lane == 0)
+                        while (bits(v_c[tl1 & (RING - 1)]) != free_tag) __nanosleep(LP_SWEEP_SLEEP);
+                    __syncwarp();
+                    const double rq = __shfl_sync(0xffffffff, rhs_t, q);
+                    if (lane < nr) {
+                        v_c[(t0 + lane) & (RING - 1)] = canon(rq - acc);
+#ifdef LP_SWEEP_TRACE
+                        if (a.trace && t0 + lane == K / 2) a.trace[(size_t)tl * 16 + 8] = gtime();
+#endif
+                    }
+                }
+                stage_base += ns;
+                continue;
+            }
             // The lex-latest line of the producers' stencil in each earlier row of
             // lines: once its value at the frontier x is visible, everything the
             // row needs has almost certainly been produced (per-value sentinel
@@ -345,9 +720,12 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                     const unsigned long long free_tag = bits(ring_sent(t));
                     while (bits(v_c[slot]) != free_tag) __nanosleep(LP_SWEEP_SLEEP);
                     v_c[slot] = canon(rhs_i - acc);
+#ifdef LP_SWEEP_TRACE
+                    if (a.trace && t == K / 2) a.trace[(size_t)tl * 16 + 8] = gtime();
+#endif
                 }
             };
-            int t = warp;
+            int t = pw;
             load_v(t, va, ra, 0);
             while (t < K) {
                 load_v(t + NP, vb, rb, 0);
@@ -362,27 +740,54 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
     }
 }
 
-// band[row] = [ in-line: M(row, row-1-q) or M(row, row+1+q), q < r |
-//               line -/+1: M(row, slot(ox, -/+1)), ox = -r..r | pad ],  rdiag = 1/U_tt
-__global__ void band_kernel(Geom g, const double *__restrict__ lu, int bs, double *__restrict__ blo,
-                            double *__restrict__ bup, double *__restrict__ rdg) {
+// Band arrays, section-major: [n][nq] in-line sections, then [n][gsz] group sections
+// (each staged by contiguous TMA bulk copies), in the sweep's step order:
+//   [0, nq):   e_1, rd, e_2, .., e_{nq-1}: e_j is the coefficient by which y(row) enters
+//              the row j steps later on the same line (fwd: L(ix+j, ix); bwd:
+//              U(ix-j, ix) / U(ix-j, ix-j)), 0 beyond r or the line end; rd = fwd 1,
+//              bwd 1/U(ix, ix);
+//   [nq, nq + 2r + 1): the coefficients by which y(line L-/+1, x = ix) enters the rows
+//              of line L that are j = 0..2r steps after its arrival step
+//              (fwd: rows x-r+j, slot (r-j, -1); bwd: rows x+r-j, slot (j-r, +1)).
+__global__ void band_kernel(Geom g, const double *__restrict__ lu, int nq, int gsz,
+                            double *__restrict__ blo, double *__restrict__ bup,
+                            double *__restrict__ rdg) {
+    const int bs = nq + gsz;
     const int64_t total = g.n * bs;
+    const int K = g.K, r = g.r;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
          q += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = q / bs;
         const int l = (int)(q % bs);
+        const int ix = (int)(i % K);
+        const int64_t row0 = i - ix;
         const double *row = lu + (size_t)i * g.S;
         double lo = 0.0, up = 0.0;
-        if (l < g.r) {
-            lo = row[g.c - 1 - l];
-            up = row[g.c + 1 + l];
-        } else if (g.d > 1 && l < 3 * g.r + 1) {
-            const int j = l - g.r;   // ox = j - r
-            lo = row[g.c - g.W - g.r + j];
-            up = row[g.c + g.W - g.r + j];
+        size_t o;
+        if (l < nq) {
+            o = (size_t)i * nq + l;
+            if (l == 1) {
+                lo = 1.0;
+                up = 1.0 / row[g.c];
+            } else {
+                const int j = l == 0 ? 1 : l;
+                if (j <= r && ix + j < K) lo = lu[(size_t)(i + j) * g.S + g.c - j];
+                if (j <= r && ix - j >= 0) {
+                    const double *rj = lu + (size_t)(i - j) * g.S;
+                    up = rj[g.c + j] * (1.0 / rj[g.c]);
+                }
+            }
+        } else {
+            const int j = l - nq;
+            o = (size_t)g.n * nq + (size_t)i * gsz + j;
+            if (g.d > 1 && j < 2 * r + 1) {
+                const int ixf = ix - r + j, ixb = ix + r - j;
+                if (ixf >= 0 && ixf < K) lo = lu[(size_t)(row0 + ixf) * g.S + g.c - g.W + r - j];
+                if (ixb >= 0 && ixb < K) up = lu[(size_t)(row0 + ixb) * g.S + g.c + g.W + j - r];
+            }
         }
-        blo[q] = lo;
-        bup[q] = up;
+        blo[o] = lo;
+        bup[o] = up;
         if (l == 0) rdg[i] = 1.0 / row[g.c];
     }
 }
@@ -405,29 +810,37 @@ int prefill(int64_t n, double *a, double *b, cudaStream_t st) {
     return LP_OK;
 }
 
-int band_stride(const Geom &g) { return (int)round_up(3 * g.r + 1, 2); }
+int band_nq(const Geom &g) { return g.r <= 7 ? 8 : 16; }
+int band_gsz(const Geom &g) { return g.d > 1 ? (int)round_up(2 * g.r + 1, 2) : 0; }
+int band_stride(const Geom &g) { return band_nq(g) + band_gsz(g); }
 
-template <bool FWD, int CH>
+template <bool FWD, int CH, int NQ>
 int run_sweep(const SweepArgs &a, const Geom &g, size_t smem, cudaStream_t st) {
     constexpr int NW = 16;
     static int nblocks = 0;
     static size_t smem_set = 0;
+    auto kern = box_sweep_kernel<FWD, NW, CH, NQ>;
     if (smem_set < smem) {
-        LP_CUDA(cudaFuncSetAttribute(box_sweep_kernel<FWD, NW, CH>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        LP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 1, dev = 0, nsm = 148;
         LP_CUDA(cudaGetDevice(&dev));
         LP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, box_sweep_kernel<FWD, NW, CH>,
-                                                              32 * NW, smem));
+        LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * NW, smem));
         nblocks = occ * nsm;
         smem_set = smem;
     }
     const int blocks = g.nlines < nblocks ? g.nlines : nblocks;
-    box_sweep_kernel<FWD, NW, CH><<<blocks, 32 * NW, smem, st>>>(a);
+    kern<<<blocks, 32 * NW, smem, st>>>(a);
     count_launch();
     LP_CHECK_LAUNCH();
     return LP_OK;
+}
+
+template <bool FWD, int NQ>
+int launch_nq(const SweepArgs &a, const Geom &g, size_t smem, cudaStream_t st) {
+    if (a.nslot <= 32 * 8) return run_sweep<FWD, 8, NQ>(a, g, smem, st);
+    if (a.nslot <= 32 * 13) return run_sweep<FWD, 13, NQ>(a, g, smem, st);
+    return run_sweep<FWD, 16, NQ>(a, g, smem, st);
 }
 
 template <bool FWD>
@@ -438,11 +851,12 @@ int launch_sweep(lp_ilu *m, const double *rhs, double *out, cudaStream_t st) {
     a.g = g;
     a.lu = m->box.lu;
     a.band = FWD ? m->box.band_lo : m->box.band_up;
-    a.rdiag = m->box.diag;
     a.rhs = rhs;
     a.out = out;
     a.ticket = m->ticket + (FWD ? 0 : 1);
-    a.bs = band_stride(g);
+    const int nq = band_nq(g);
+    a.gsz = band_gsz(g);
+    a.band_g = a.band + (size_t)g.n * nq;
     // producers: everything except the in-line entries and (d >= 2) line -/+1
     const int excl = g.d > 1 ? g.W + g.r : g.r;
     a.lo = FWD ? 0 : g.c + excl + 1;
@@ -452,9 +866,9 @@ int launch_sweep(lp_ilu *m, const double *rhs, double *out, cudaStream_t st) {
     {
         static unsigned long long *tr = nullptr;
         static size_t trn = 0;
-        if (trn < (size_t)g.nlines * 4) {
+        if (trn < (size_t)g.nlines * 16) {
             if (tr) dfree(tr);
-            trn = (size_t)g.nlines * 4;
+            trn = (size_t)g.nlines * 16;
             dalloc(&tr, trn, "sweep trace");
         }
         cudaMemsetAsync(tr, 0, trn * 8, st);
@@ -463,12 +877,19 @@ int launch_sweep(lp_ilu *m, const double *rhs, double *out, cudaStream_t st) {
         g_trace_n = trn;
     }
 #endif
-    const size_t smem = (size_t)BRING * a.bs * sizeof(double) + BRING * sizeof(double) +
-                        (size_t)a.nslot * (sizeof(int) + 4) + 16;
+    size_t smem = (size_t)BRING * (nq + a.gsz) * sizeof(double) + (size_t)a.nslot * (sizeof(int) + 4);
+    smem = (size_t)round_up((int64_t)smem, 16);
+    a.pr_ofs = (unsigned)smem;
+    a.nseg = g.d == 2 ? g.r - 1 : 0;
+    a.pr_rs = (int)round_up(a.nslot + 1, 2);
+    a.pr_ww = (int)round_up(PR + 2 * g.r, 2);
+    if (g.d == 2)
+        smem += (size_t)NSTAGE * (PR * a.pr_rs + a.nseg * a.pr_ww) * sizeof(double) +
+                (size_t)a.nslot * sizeof(int);
+    smem += 16;
+    LP_ARG(smem <= 227 * 1024, "sweep needs %zu bytes of shared memory (reach %d)", smem, g.r);
     LP_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(int), st));
-    if (a.nslot <= 32 * 8) return run_sweep<FWD, 8>(a, g, smem, st);
-    if (a.nslot <= 32 * 13) return run_sweep<FWD, 13>(a, g, smem, st);
-    return run_sweep<FWD, 16>(a, g, smem, st);
+    return nq == 8 ? launch_nq<FWD, 8>(a, g, smem, st) : launch_nq<FWD, 16>(a, g, smem, st);
 }
 
 }  // namespace
@@ -482,7 +903,7 @@ int box_build_bands(lp_ilu *m, cudaStream_t st) {
                        (rc = dalloc(&b.band_up, (size_t)b.n * bs, "band")) ||
                        (rc = dalloc(&b.diag, (size_t)b.n, "diag"))))
         return rc;
-    band_kernel<<<148 * 8, 256, 0, st>>>(g, b.lu, bs, b.band_lo, b.band_up, b.diag);
+    band_kernel<<<148 * 8, 256, 0, st>>>(g, b.lu, band_nq(g), band_gsz(g), b.band_lo, b.band_up, b.diag);
     count_launch();
     LP_CHECK_LAUNCH();
     return LP_OK;
@@ -507,6 +928,11 @@ int box_apply(lp_ilu *m, const double *r, double *z, cudaStream_t st) {
 }
 
 }  // namespace lp
+
+extern "C" int lp_debug_sweep_check(long long *host) {
+    cudaDeviceSynchronize();
+    return cudaMemcpyFromSymbol(host, lp::g_chk, 8 * sizeof(long long)) == cudaSuccess ? 0 : -1;
+}
 
 extern "C" int lp_debug_sweep_trace(unsigned long long *host, int64_t n) {
     if (!lp::g_trace) return -1;

@@ -477,7 +477,8 @@ int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st) {
     }
     const size_t bytes = (size_t)b.n * b.S * sizeof(double);
     if (!b.lu) {
-        if (dalloc(&b.lu, (size_t)b.n * b.S, "ILU factors") != LP_OK) {
+        // +2 doubles: the sweeps stage factor rows with 16-byte aligned bulk copies
+        if (dalloc(&b.lu, (size_t)b.n * b.S + 2, "ILU factors") != LP_OK) {
             // not enough memory for a separate copy: factor in place, drop M
             b.lu = b.values;
             b.values = nullptr;
@@ -659,7 +660,7 @@ extern "C" int lp_box_assemble(int d, int K, int n_groups, const int *lens, cons
         lp_ilu_destroy(m);
         return code;
     };
-    if ((rc = dalloc(&b.values, (size_t)b.n * b.S, "preconditioner values")) ||
+    if ((rc = dalloc(&b.values, (size_t)b.n * b.S + 2, "preconditioner values")) ||
         (rc = dalloc(&b.mask, (size_t)b.n * b.mask_words, "pattern bits")) ||
         (rc = dalloc(&dhats, hat_total, "hats")) || (rc = dalloc(&dblocks, nblk, "1-D blocks")) ||
         (rc = dalloc(&cnt, 2, "counters")) ||

@@ -23,10 +23,12 @@ for _ in range(3):
     lib.lp_forward_sub(f._handle, r.data_ptr(), y.data_ptr(), _lib.stream_ptr())
 torch.cuda.synchronize()
 nl = n // w.K
-buf = np.zeros(nl * 4, dtype=np.uint64)
+buf = np.zeros(nl * 16, dtype=np.uint64)
 lib.lp_debug_sweep_trace.restype = ctypes.c_int
 lib.lp_debug_sweep_trace(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_int64(buf.size))
-t = buf.reshape(nl, 4).astype(np.int64)
+tc = buf.reshape(nl, 16).astype(np.int64)
+t = tc[:, :4]
+cy = tc[:, 4:]
 t0 = t[:, 0].min()
 t = (t - t0) / 1e3
 print(name, "line  start  row0  rowmid  rowlast   (us)")
@@ -35,3 +37,17 @@ for L in list(range(0, 12)) + list(range(nl // 2, nl // 2 + 4)) + list(range(nl 
 d0 = np.diff(t[:, 1])
 print("lead (row0 to row0) median us", np.median(d0), "line duration median",
       np.median(t[:, 3] - t[:, 1]), "start->row0 median", np.median(t[:, 1] - t[:, 0]))
+half = w.K - 1 - w.K // 2
+cps = (cy[:, 3] - cy[:, 2]) / half
+nsps = (t[:, 3] - t[:, 2]) / half
+print("second-half-of-line cycles/step: line0", cps[0], "median", np.median(cps),
+      "| ns/step line0", nsps[0] * 1e3, "median", np.median(nsps) * 1e3,
+      "| implied MHz", np.median(cps / (nsps * 1e3)) * 1e3)
+print("serial cycles waiting for band chunks per line: line0", cy[0, 0], "median", np.median(cy[:, 0]))
+ev = (tc[:, 8:11] - t0) / 1e3   # producer c_mid, group d_mid, group arrival at mid (us)
+print("mid-row events (us): line  c_mid(prod)  arrival(grp)  d_mid(grp)  y_mid(serial)")
+for L in list(range(0, 6)) + [nl // 2]:
+    print(L, *[f"{v:9.2f}" for v in (ev[L, 0], ev[L, 2], ev[L, 1], t[L, 2])])
+print("group loop cycles/step (median over lines)", np.median(tc[1:, 11] / (w.K + w.T + 2)),
+      "| group re-polls per line: median", np.median(tc[1:, 12]), "max", tc[1:, 12].max(),
+      "| serial spins on c per line", np.median(tc[:, 13]), "on A", np.median(tc[1:, 14]))
