@@ -94,6 +94,20 @@ __device__ __forceinline__ void sts_v(unsigned a, double v) {
     asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 
+// A value the compiler must keep in a register (it cannot rematerialise it from
+// the parameter bank, which it otherwise does every iteration of a loop that
+// contains "memory"-clobbering inline asm).
+__device__ __forceinline__ int opaque(int v) {
+    int r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+__device__ __forceinline__ unsigned opaque(unsigned v) {
+    unsigned r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+
 __device__ __forceinline__ double ring_sent(int t) {
     return __longlong_as_double((long long)(RING_SENT | (unsigned)t));
 }
@@ -363,11 +377,13 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                 wait_chunk(c + 1);
                 const int t1 = min(32 * c + 32, Kr);
 #ifdef LP_SWEEP_TRACE
-                const int th = Kr / 2;
-                if (32 * c <= th && th < t1) {
-                    for (int t = 32 * c; t < th; ++t) step(t);
-                    mark(2);
-                    for (int t = th; t < t1; ++t) step(t);
+                const int th = Kr / 2, th2 = Kr / 2 + r + 1;
+                if ((32 * c <= th && th < t1) || (32 * c <= th2 && th2 < t1)) {
+                    for (int t = 32 * c; t < t1; ++t) {
+                        if (t == th) mark(2);
+                        if (t == th2 && lane == 0 && a.trace) a.trace[(size_t)tl * 16 + 15] = gtime();
+                        step(t);
+                    }
                     continue;
                 }
 #endif
@@ -415,79 +431,67 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
             stage(1);
             stage(2);
             wait_chunk(0);
-            const int tw = 2 * R;
+            // loop constants in registers (opaque: no per-step parameter-bank reloads)
+            const int Kr = opaque(K), tw = opaque(2 * R);
+            const unsigned gstr = opaque(gstride);
             double acc = 0.0;
-            double yb = 0.0;   // lane l: y(L-/+1, arrival index (uarr & ~31) + l)
-            double ybn = 0.0;  // the next block's values, polled half a block early
+            double yb = 0.0;   // lane l: y(L-/+1, arrival index 32 b + l)
             auto poll_block = [&](int u0) -> double {
                 const int ua = u0 + lane;
-                return (has_prev && ua < K) ? ld_poll(prev + (FWD ? ua : K - 1 - ua)) : 0.0;
+                return ua < Kr ? ld_poll(prev + (FWD ? ua : Kr - 1 - ua)) : 0.0;
             };
-            // coefficient of arrival u for this lane's row (band row x(u), j = row - (u - R))
-            auto coef = [&](int u) -> double {
-                const int x = FWD ? u : K - 1 - u;
-                const int j = (lane - (u - R)) & 31;
-                return (u < K && j <= tw) ? lds(grp0 + (x & (BRING - 1)) * gstride + 8 * j) : 0.0;
-            };
-            int Kr;
-            asm volatile("mov.b32 %0, %1;" : "=r"(Kr) : "r"(K));
-            if (has_prev) ybn = poll_block(0);
-            double qn = 0.0, ynx = 0.0;   // the current step's coefficient and value
+            double ybn = poll_block(0);   // the next block's values, polled half a block early
+            const unsigned jl0 = (unsigned)(lane + R) & 31;   // j = (jl0 - i) & 31 at step i of a block
 #ifdef LP_SWEEP_TRACE
             const long long gc0 = clock64();
             long long nrepoll = 0;
 #endif
-            for (int t = -R; t < Kr; ++t) {
-                const int uarr = t + R;   // arrival index
-                const int t32 = uarr & 31;
-                if (t32 == 0) {
-                    stage((uarr >> 5) + 3);
-                    wait_chunk((uarr >> 5) + 1);
-                    yb = ybn;
-                    // the serial has consumed every slot this block will write
-                    if (t >= 0) {
-                        const int tl31 = t + 31;
+            const int nblk = (Kr + R + 31) / 32;
+            for (int blk = 0; blk < nblk; ++blk) {
+                const int u0 = 32 * blk;
+                stage(blk + 3);
+                wait_chunk(blk + 1);
+                yb = ybn;
+                // the serial has consumed every slot this block will write
+                {
+                    const int tl31 = u0 + 31 - R;
+                    if (tl31 >= 0) {
                         const unsigned long long fb = bits(ring_sent(tl31));
                         while (bits(lds_v(d0 + (tl31 & (RING - 1)) * 8)) != fb) {
                         }
                     }
-                    __syncwarp();
-                    if (has_prev) {
-                        ynx = __shfl_sync(0xffffffff, yb, 0);
-                        qn = coef(uarr);
-                    }
-                } else if (t32 == 16 && has_prev) {
-                    ybn = poll_block(uarr + 16);
                 }
-                if (has_prev && uarr < Kr) {
-                    double yn = ynx;
-                    while (bits(yn) == SWEEP_SENTINEL) {
-                        // re-poll the rest of the window: one round trip brings in
-                        // every value produced since the last poll
-                        const int ua = uarr - t32 + lane;
-                        if (lane >= t32 && ua < Kr) yb = ld_poll(prev + (FWD ? ua : Kr - 1 - ua));
-                        yn = __shfl_sync(0xffffffff, yb, t32);
+                __syncwarp();
+                double ynx = __shfl_sync(0xffffffff, yb, 0);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int uarr = u0 + i, t = uarr - R;
+                    if (i == 16) ybn = poll_block(u0 + 32);
+                    if (uarr < Kr) {
+                        double yn = ynx;
+                        while (bits(yn) == SWEEP_SENTINEL) {
+                            // re-poll the rest of the window: one round trip brings in
+                            // every value produced since the last poll
+                            const int ua = u0 + lane;
+                            if (lane >= i && ua < Kr) yb = ld_poll(prev + (FWD ? ua : Kr - 1 - ua));
+                            yn = __shfl_sync(0xffffffff, yb, i);
 #ifdef LP_SWEEP_TRACE
-                        ++nrepoll;
+                            ++nrepoll;
 #endif
+                        }
+#ifdef LP_SWEEP_TRACE
+                        if (lane == 0 && a.trace && t == K / 2) a.trace[(size_t)tl * 16 + 10] = gtime();
+#endif
+                        const int x = FWD ? uarr : Kr - 1 - uarr;
+                        const unsigned j = (jl0 - (unsigned)i) & 31;
+                        const double q = (int)j <= tw ? lds(grp0 + (unsigned)(x & (BRING - 1)) * gstr + 8 * j) : 0.0;
+                        if (i < 31) ynx = __shfl_sync(0xffffffff, yb, i + 1);
+                        acc = fma(q, yn, acc);
                     }
-#ifdef LP_SWEEP_TRACE
-                    if (lane == 0 && a.trace && t == K / 2) a.trace[(size_t)tl * 16 + 10] = gtime();
-#endif
-                    acc = fma(qn, yn, acc);
-                    if (t32 < 31) {   // next step's operands, off this step's path
-                        ynx = __shfl_sync(0xffffffff, yb, t32 + 1);
-                        qn = coef(uarr + 1);
+                    if (lane == ((i - R) & 31) && t >= 0 && t < Kr) {
+                        sts_v(d0 + (unsigned)(t & (RING - 1)) * 8, acc);
+                        acc = 0.0;
                     }
-                }
-                if (t >= 0 && lane == (t & 31)) {
-                    sts_v(d0 + (unsigned)(t & (RING - 1)) * 8, acc);
-                    acc = 0.0;
-                }
-                if (t >= 0) {
-#ifdef LP_SWEEP_TRACE
-                    if (lane == 0 && a.trace && t == K / 2) a.trace[(size_t)tl * 16 + 9] = gtime();
-#endif
                 }
             }
 #ifdef LP_SWEEP_TRACE
@@ -538,6 +542,20 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                     // slot free: stage gs - NSTAGE (the previous user) consumed
                     while (v_cons[slot] < gs / NSTAGE) {
                     }
+#ifdef LP_EXP_NOPROD
+                    if (true) {
+                        if (lane < nr) {
+                            const int ix = FWD ? t0 + lane : K - 1 - t0 - lane;
+                            const double rv = a.rhs[row0 + ix];
+                            const int tl1 = t1 - 1;
+                            while (bits(v_c[tl1 & (RING - 1)]) != bits(ring_sent(tl1))) __nanosleep(LP_SWEEP_SLEEP);
+                            v_c[(t0 + lane) & (RING - 1)] = rv;
+                        }
+                        __syncwarp();
+                        if (lane == 0) v_cons[slot] = gs / NSTAGE + 1;
+                        continue;
+                    }
+#endif
                     // factor rows: one 16-byte aligned bulk copy per row
                     if (lane == 0) {
                         unsigned bytes = 0;

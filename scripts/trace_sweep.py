@@ -51,3 +51,15 @@ for L in list(range(0, 6)) + [nl // 2]:
 print("group loop cycles/step (median over lines)", np.median(tc[1:, 11] / (w.K + w.T + 2)),
       "| group re-polls per line: median", np.median(tc[1:, 12]), "max", tc[1:, 12].max(),
       "| serial spins on c per line", np.median(tc[:, 13]), "on A", np.median(tc[1:, 14]))
+# y(L-1, K/2 + r) is produced just before line L-1's step K/2 + r + 1 is marked
+prod = (tc[:, 15] - t0) / 1e3
+arr = ev[:, 2]
+lam = arr[1:] - prod[:-1]
+print("detect latency y(L-1, mid+r) produced -> seen by line L's group (us): median", np.median(lam),
+      "p10", np.percentile(lam, 10), "p90", np.percentile(lam, 90))
+print("arrival -> y_mid of line L (us): median", np.median(t[1:, 2] - arr[1:]))
+print("line-L-1 r steps (y_mid -> y_mid+r) (us): median", np.median(prod - t[:, 2]))
+slope = (t[:, 3] - t[:, 2]) / half * 1e3
+print("per-line slope ns/step (lines 0..15):", " ".join(f"{v:.0f}" for v in slope[:16]))
+print("per-line detect latency us (lines 1..15):", " ".join(f"{v:.2f}" for v in lam[:15]))
+print("slope ns/step at lines 50,100,150,200,250:", " ".join(f"{slope[i]:.0f}" for i in (50, 100, 150, 200, 250) if i < nl))
