@@ -90,9 +90,13 @@ def _offsets(kind, t):
     return [o for o in range(-reach, reach + 1) if (o - t) % 2 == 0]
 
 
+_BLOCKS = {}
+
+
 def building_blocks_1d(T, K, plan):
     """Exact-quadrature diagonals of S^(t) = (L_t phi', phi') and
-    M^(t) = (L_t phi, phi), t = 0..T (precond.py:118-161)."""
+    M^(t) = (L_t phi, phi), t = 0..T (precond.py:118-161).  Memoised per
+    (T, K, rule); the diagonals are read-only."""
     if T < 0 or K < 1:
         raise ValueError("need T >= 0 and K >= 1")
     rule = plan if isinstance(plan, GaussRule) else plan.rule
@@ -100,6 +104,19 @@ def building_blocks_1d(T, K, plan):
     if rule.order < needed:
         raise ValueError(f"quadrature order {rule.order} is insufficient for exact "
                          f"blocks with T={T}, K={K}: need at least {needed}")
+    key = (int(T), int(K), rule.nodes.tobytes(), rule.weights.tobytes())
+    hit = _BLOCKS.get(key)
+    if hit is None:
+        hit = _building_blocks_1d(int(T), int(K), rule)
+        for bl in hit:
+            for b in bl:
+                for dg in b.diags.values():
+                    dg.flags.writeable = False
+        _BLOCKS[key] = hit
+    return hit
+
+
+def _building_blocks_1d(T, K, rule):
     acc = {kind: [{o: np.zeros(K) for o in _offsets(kind, t)} for t in range(T + 1)]
            for kind in ("stiff", "mass")}
     dcoef = -(2.0 * np.arange(K) + 3.0)
@@ -125,7 +142,17 @@ def building_blocks_1d(T, K, plan):
 
 
 def _groups(spec, t1, t2):
-    """(hat, stiff axis or None) terms (precond.py:175-197)."""
+    """(hat, stiff axis or None) terms (precond.py:175-197), cached on the spec
+    (its coefficient fields are fixed)."""
+    key = ("groups", tuple(t1) if isinstance(t1, (tuple, list)) else t1, t2)
+    hit = spec._op_cache.get(key)
+    if hit is None:
+        hit = _groups_uncached(spec, t1, t2)
+        spec._op_cache[key] = hit
+    return hit
+
+
+def _groups_uncached(spec, t1, t2):
     d = spec.dim
     out = []
     if spec.axis_betas is not None:

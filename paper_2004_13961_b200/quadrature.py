@@ -40,12 +40,28 @@ def _value_and_slope(n, x):
     return cur, n * (prev - x * cur) / (1.0 - x * x)
 
 
+_RULES = {}
+
+
 def gauss_rule(order, tol=1e-15, max_iter=100):
     """Nodes (increasing) and weights of the order-P Legendre-Gauss rule.
 
     Newton iteration from cos(pi (4k+3)/(4P+2)) with
     (1 - x^2) L_P' = P (L_{P-1} - x L_P), one polishing step, then exact
-    antisymmetrisation of the nodes and symmetrisation of the weights."""
+    antisymmetrisation of the nodes and symmetrisation of the weights.
+    Rules are memoised (read-only arrays): every solve's setup asks for the
+    same few orders."""
+    key = (int(order), float(tol), int(max_iter))
+    rule = _RULES.get(key)
+    if rule is None:
+        rule = _gauss_rule(*key)
+        rule.nodes.flags.writeable = False
+        rule.weights.flags.writeable = False
+        _RULES[key] = rule
+    return rule
+
+
+def _gauss_rule(order, tol, max_iter):
     P = int(order)
     if P < 1:
         raise ValueError("order must be >= 1")
