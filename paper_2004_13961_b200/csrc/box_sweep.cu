@@ -32,6 +32,7 @@
 
 #include "box_geom.cuh"
 #include "ilu.cuh"
+#include "smem_tma.cuh"
 
 namespace lp {
 
@@ -71,42 +72,17 @@ __device__ __forceinline__ double ld_poll(const double *p) {
 
 // Shared-memory accesses through 32-bit shared-window addresses (computed once;
 // generic pointers make the compiler re-derive the window base every step).
-__device__ __forceinline__ unsigned smem_addr(const void *p) {
-    unsigned a;
-    // opaque to the compiler, so the value stays in a register
-    asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(a) : "l"(p));
-    return a;
-}
-__device__ __forceinline__ double lds(unsigned a) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void lds2(unsigned a, double &x, double &y) {
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
-}
-__device__ __forceinline__ double lds_v(unsigned a) {
-    double v;
-    asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts_v(unsigned a, double v) {
-    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
-}
+
+
+
+
+
 
 // A value the compiler must keep in a register (it cannot rematerialise it from
 // the parameter bank, which it otherwise does every iteration of a loop that
 // contains "memory"-clobbering inline asm).
-__device__ __forceinline__ int opaque(int v) {
-    int r;
-    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
-    return r;
-}
-__device__ __forceinline__ unsigned opaque(unsigned v) {
-    unsigned r;
-    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
-    return r;
-}
+
+
 
 __device__ __forceinline__ double ring_sent(int t) {
     return __longlong_as_double((long long)(RING_SENT | (unsigned)t));
@@ -150,23 +126,11 @@ __device__ __forceinline__ unsigned long long gtime() {
     return t;
 }
 
-__device__ __forceinline__ void mbar_init(unsigned a, unsigned cnt) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(unsigned a, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned bytes, unsigned mbar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned a) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
-    asm volatile("{\n .reg .pred p;\n LP_W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-                 " @!p bra LP_W%=;\n}" ::"r"(a), "r"(parity) : "memory");
-}
+
+
+
+
+
 
 // One TMA bulk copy (two at the ring wrap) of the w-double rows of steps
 // [32c, 32c + 32) of a line into a BRING-row shared ring (ring row = ix mod BRING),

@@ -58,4 +58,6 @@ int box_spmv(lp_ilu *m, const double *x, double *y, cudaStream_t st);
 int box_export(const lp_ilu *m, int which, int64_t *indptr, int32_t *indices, double *values);
 int box_build_bands(lp_ilu *m, cudaStream_t st);
 int box_apply(lp_ilu *m, const double *r, double *z, cudaStream_t st);
+int box_ilu0_2d_tasks(lp_ilu *m, double tol, unsigned long long *key, const unsigned char *full,
+                      int *edone, cudaStream_t st);
 }  // namespace lp

@@ -510,7 +510,28 @@ int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st) {
     // (Measured on B200: cfg 2, K (r+1) = 3315 -> row kernel 57 ms vs line kernel
     // 198 ms; cfg 3, K (r+1) = 30705 -> row kernel 9.5 s vs line kernel 3.1 s.)
     const bool window_ok = (int64_t)g.K * (g.r + 1) <= 8192;
-    if (g.d <= 2 && !window_ok && g.r + 1 <= LNW && line_smem <= 220 * 1024) {
+    bool done = false;
+    if (g.d == 2) {
+        // task-graph factorisation (ilu_box2d.cu)
+        unsigned char *full = nullptr;
+        int *edone = nullptr;
+        const int nb = (g.K + 15) / 16;
+        int rcf;
+        if ((rcf = dalloc(&full, (size_t)b.n, "full-row flags"))) return rcf;
+        if ((rcf = dalloc(&edone, (size_t)g.nlines * nb, "task flags"))) return rcf;
+        LP_CUDA(cudaMemsetAsync(edone, 0, (size_t)g.nlines * nb * sizeof(int), st));
+        box_full_kernel<<<148 * 8, 256, 0, st>>>(g, b.mask, full);
+        count_launch();
+        const int rt = box_ilu0_2d_tasks(m, tol, key, full, edone, st);
+        if (rt == LP_OK) {
+            LP_CUDA(cudaStreamSynchronize(st));
+            done = true;
+        }
+        dfree(full);
+        dfree(edone);
+    }
+    if (done) {
+    } else if (g.d <= 2 && !window_ok && g.r + 1 <= LNW && line_smem <= 220 * 1024) {
         LP_CUDA(cudaFuncSetAttribute(box_ilu0_line_kernel<LNW>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)line_smem));
         int occ = 1;
@@ -546,7 +567,7 @@ int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st) {
         box_ilu0_kernel<256><<<(unsigned)blocks, 256, smem, st>>>(g, b.lu, b.mask, m->flags, epoch,
                                                                  m->ticket, tol, key);
     }
-    count_launch();
+    if (!done) count_launch();
     LP_CHECK_LAUNCH();
     unsigned long long hk;
     double plast;

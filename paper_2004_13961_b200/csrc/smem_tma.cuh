@@ -1,0 +1,69 @@
+// Shared-memory, TMA bulk-copy and mbarrier helpers (inline PTX, sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace lp {
+
+__device__ __forceinline__ unsigned smem_addr(const void *p) {
+    unsigned a;
+    // opaque to the compiler, so the value stays in a register
+    asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(a) : "l"(p));
+    return a;
+}
+
+__device__ __forceinline__ double lds(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+
+__device__ __forceinline__ void lds2(unsigned a, double &x, double &y) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+
+__device__ __forceinline__ double lds_v(unsigned a) {
+    double v;
+    asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void sts_v(unsigned a, double v) {
+    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ int opaque(int v) {
+    int r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+
+__device__ __forceinline__ unsigned opaque(unsigned v) {
+    unsigned r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+
+__device__ __forceinline__ void mbar_init(unsigned a, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect(unsigned a, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned bytes, unsigned mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
+    asm volatile("{\n .reg .pred p;\n LP_W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 " @!p bra LP_W%=;\n}" ::"r"(a), "r"(parity) : "memory");
+}
+
+}  // namespace lp
