@@ -143,26 +143,65 @@ def dgemm_tflops(torch):
     return 2.0 * n ** 3 / best / 1e12
 
 
-def sweep_traffic(workload):
-    """DRAM bytes (read + write) of one precond_apply (two box_sweep_kernel launches)
-    from the committed ncu --set full capture (profiles/r01_box_sweep_full.csv, cfg 2)."""
-    if workload != "cfg2":
-        return None
-    path = os.path.join(ROOT, "profiles", "r01_box_sweep_full.csv")
+PROFILE_TAG = "r01b"
+
+
+def _ncu_rows(name):
+    """Rows (dicts) of a committed ncu --set full summary: profiles/<tag>_<name>_full.csv."""
+    import csv
+    path = os.path.join(ROOT, "profiles", f"{PROFILE_TAG}_{name}_full.csv")
     try:
-        import csv
-        tot = 0.0
         with open(path) as f:
-            for row in csv.reader(f):
-                if len(row) >= 4 and "box_sweep_kernel" in row[0] and not row[0].startswith("#"):
-                    tot += (float(row[2]) + float(row[3])) * 1e6   # Mbyte
-        return tot or None
-    except (OSError, ValueError, IndexError):
+            lines = [ln for ln in f if not ln.startswith("#")]
+    except OSError:
+        return []
+    rows = list(csv.reader(lines))
+    if len(rows) < 3:
+        return []
+    return [dict(zip(rows[0], r)) for r in rows[2:]]
+
+
+def ncu_traffic(name, kernel, per_call=1):
+    """DRAM bytes (read + write) per call of `kernel` from the committed capture (cfg 2),
+    summed over `per_call` consecutive launches (a precond_apply is 2 sweep launches)."""
+    rows = [r for r in _ncu_rows(name) if kernel in r.get("Kernel Name", "")]
+    if not rows:
         return None
+    try:
+        per = [float(r["dram__bytes_read.sum"]) + float(r["dram__bytes_write.sum"]) for r in rows]
+    except (KeyError, ValueError):
+        return None
+    return sum(per) / len(per) * per_call
+
+
+def sweep_traffic(workload):
+    """DRAM bytes of one precond_apply (fwd + bwd box_sweep_kernel) from the committed capture."""
+    return ncu_traffic("sweep", "box_sweep_kernel", 2) if workload == "cfg2" else None
 
 
 def flush_l2(torch, buf):
     buf.zero_()
+
+
+def ilu_flops(w):
+    """F_ilu = 2 x (in-pattern IKJ updates), interior-row count x rows (SURVEY 8(d):
+    73,008 / 132,300 updates per interior row for r = 12 / 14 in 2-D)."""
+    r = w.T + 2
+    if w.dim == 2:
+        W = 2 * r + 1
+        # updates of an interior row: pivots (ox, oy) < 0, targets in both boxes past k
+        upd = 0
+        for oy in range(-r, 1):
+            for ox in range(-r, r + 1):
+                if oy == 0 and ox >= 0:
+                    break
+                for ty in range(oy, min(r, oy + r) + 1):
+                    for tx in range(max(-r, ox - r), min(r, ox + r) + 1):
+                        if ty == oy and tx <= ox:
+                            continue
+                        upd += 1
+        return 2.0 * upd * w.dofs
+    return None
 
 
 def matvec_flops(d, P, K):
@@ -259,14 +298,16 @@ def run_b200(args, ws, rank, local):
     t_setup = time.perf_counter() - t_setup0
     from paper_2004_13961_b200.precond import assemble_M
     from paper_2004_13961_b200.sparse import ilu0
-    ta0 = time.perf_counter()
-    m = assemble_M(spec, w.T, w.T, plan)
-    torch.cuda.synchronize()
-    t_asm = time.perf_counter() - ta0
-    tf0 = time.perf_counter()
-    ilu0(m)
-    torch.cuda.synchronize()
-    t_fac = time.perf_counter() - tf0
+    # second of two calls: the first pays one-time module loading / attribute setup
+    for _ in range(2):
+        ta0 = time.perf_counter()
+        m = assemble_M(spec, w.T, w.T, plan)
+        torch.cuda.synchronize()
+        t_asm = time.perf_counter() - ta0
+        tf0 = time.perf_counter()
+        ilu0(m)
+        torch.cuda.synchronize()
+        t_fac = time.perf_counter() - tf0
     nnz = m.nnz
     r = torch.randn(n, dtype=torch.float64, device="cuda")
     z = torch.empty_like(r)
@@ -301,9 +342,13 @@ def run_b200(args, ws, rank, local):
                "achieved": mv_tf, "peak": fp64, "unit": "TFLOP/s", "frac": mv_tf / fp64,
                "traffic": None, "algorithmic_flops": F_alg,
                "peak_source": "cuBLAS DGEMM 8192^3 measured in this run"}
-    roof_fac = {"kernel": "box_ilu0_kernel", "bound": "latency",
-                "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None,
-                "seconds": t_fac}
+    F_ilu = ilu_flops(w)
+    ilu_tf = F_ilu / t_fac / 1e12 if F_ilu else None
+    roof_fac = {"kernel": "box_ilu0_tasks (2-D task graph)" if w.dim == 2 else "box_ilu0_kernel",
+                "bound": "latency (row-to-row dependency chain); fp64 rate shown",
+                "achieved": ilu_tf, "peak": fp64, "unit": "TFLOP/s", "frac": ilu_tf / fp64 if ilu_tf else None,
+                "traffic": ncu_traffic("ilu", "box_ilu0_tasks") if w.name == "cfg2" else None,
+                "algorithmic_flops": F_ilu, "seconds": t_fac}
     roof = {"sweeps": roof_sweep, "matvec": roof_mv, "ilu0": roof_fac}[dom]
     result = {
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": ws, "steps": args.steps,

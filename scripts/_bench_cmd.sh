@@ -1,4 +1,3 @@
 cd /root/repo
 python bench.py --stages > gpurun_out/bench_cfg2.json 2> gpurun_out/bench_cfg2.err
 echo EXIT $? >> gpurun_out/bench_cfg2.err
-python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/bench_ref.json 2>&1
