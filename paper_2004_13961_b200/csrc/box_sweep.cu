@@ -117,6 +117,8 @@ struct SweepArgs {
     int pr_rs, pr_ww;     // 2-D staged producers: factor row stride / y-window width (doubles)
     unsigned pr_ofs;      // byte offset of the producers' staging region in dynamic smem
     int nseg;             // 2-D: lines of the producers' stencil (r - 1)
+    int csize;            // cluster size: lines of a batch (consecutive in sweep order)
+    unsigned yr_ofs;      // byte offset of the line-handoff buffer [K] in dynamic smem
     unsigned long long *trace;   // LP_SWEEP_TRACE builds: per-line timestamps
 };
 
@@ -208,16 +210,34 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
         s_delta[j] = (sx - r) + K * ((sy - r) + K * (sz - r));
     }
 
+    // Lines are handed out in batches of csize consecutive lines, one per CTA of a
+    // cluster; each CTA pushes its y values straight into the shared memory of
+    // the CTA holding the next line (distributed shared memory), so the
+    // line-to-line handoff inside a batch skips the L2 round trips.
+    const unsigned crank = a.csize > 1 ? cluster_rank() : 0;
+    double *s_yr = reinterpret_cast<double *>(dsm + a.yr_ofs);   // [K]: y of the previous line
+    const unsigned yr0 = smem_addr(s_yr);
+    const bool use_yr = a.csize > 1;
+    const double sent = __longlong_as_double((long long)SWEEP_SENTINEL);
     for (;;) {
         __syncthreads();
-        if (tid == 0) s_line = atomicAdd(a.ticket, 1);
+        if (use_yr)
+            for (int x = tid; x < K; x += blockDim.x) s_yr[x] = sent;
+        if (crank == 0 && tid == 0) {
+            const int tb = atomicAdd(a.ticket, 1);
+            s_line = tb;
+            for (int q = 1; q < a.csize; ++q) st_cluster_s32(map_rank(smem_addr(&s_line), q), tb);
+        }
         for (int k = tid; k < RING; k += blockDim.x) {
             s_c[k] = ring_sent(k);
             s_d[k] = ring_sent(k);
         }
-        __syncthreads();
-        const int tl = s_line;
-        if (tl >= g.nlines) return;
+        if (use_yr) cluster_sync();
+        else __syncthreads();
+        const int tb = s_line;
+        if (tb * a.csize >= g.nlines) return;
+        const int tl = tb * a.csize + (int)crank;
+        if (tl >= g.nlines) continue;   // idle rank of the last batch
         const int L = FWD ? tl : g.nlines - 1 - tl;
         const int iy = g.d > 1 ? L % K : 0, iz = g.d > 2 ? L / K : 0;
         for (int j = tid; j < a.nslot; j += blockDim.x) {
@@ -282,6 +302,10 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
             int Kr;
             asm volatile("mov.b32 %0, %1;" : "=r"(Kr) : "r"(K));
             unsigned qoff = 8u * (unsigned)lane;   // 8 * ((lane - t) & 31)
+            // next line of the batch in the same plane: it reads this line's values
+            const bool push = use_yr && crank + 1 < (unsigned)a.csize && tl + 1 < g.nlines &&
+                              (g.d < 2 || (FWD ? iy < K - 1 : iy > 0));
+            const unsigned push_base = push ? map_rank(yr0, crank + 1) : 0u;
 #ifdef LP_SWEEP_TRACE
             long long nspin_c = 0, nspin_a = 0;
 #endif
@@ -311,6 +335,7 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                 if (t == Kr - 1)
 #endif
                 __stcg(outp, canon(y));
+                if (push) st_cluster_f64(push_base + 8u * (unsigned)(FWD ? t : Kr - 1 - t), canon(y));
                 outp += ostep;
                 doff = (doff + 8) & (RING * 8 - 1);
                 cn = lds_v(c0 + doff);
@@ -378,6 +403,10 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
             const bool has_prev = g.d > 1 && (FWD ? iy > 0 : iy < K - 1);
             if (!has_prev) continue;
             const double *prev = a.out + (FWD ? row0 - K : row0 + K);   // line L-/+1
+            // line L-/+2 of the same plane (produced a line earlier: always complete
+            // in the block polls, its coefficients follow the 2r+1 of line L-/+1)
+            const bool has_prev2 = FWD ? iy > 1 : iy < K - 2;
+            const double *prev2 = a.out + (FWD ? row0 - 2 * K : row0 + 2 * K);
             const int R = r;
             const unsigned gstride = (unsigned)a.gsz * 8;
             const unsigned grp0 = smem_addr(s_grp), c0 = smem_addr(s_c), d0 = smem_addr(s_d);
@@ -400,11 +429,21 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
             const unsigned gstr = opaque(gstride);
             double acc = 0.0;
             double yb = 0.0;   // lane l: y(L-/+1, arrival index 32 b + l)
+            // previous line held by the CTA before us in the cluster: its values land
+            // in our shared memory; otherwise poll them in L2
+            const bool local = use_yr && crank > 0;
+            auto pollv = [&](int x) -> double { return local ? lds_v(yr0 + 8u * (unsigned)x) : ld_poll(prev + x); };
             auto poll_block = [&](int u0) -> double {
                 const int ua = u0 + lane;
-                return ua < Kr ? ld_poll(prev + (FWD ? ua : Kr - 1 - ua)) : 0.0;
+                return ua < Kr ? pollv(FWD ? ua : Kr - 1 - ua) : 0.0;
             };
             double ybn = poll_block(0);   // the next block's values, polled half a block early
+            auto poll_block2 = [&](int u0) -> double {
+                const int ua = u0 + lane;
+                return (has_prev2 && ua < Kr) ? ld_poll(prev2 + (FWD ? ua : Kr - 1 - ua)) : 0.0;
+            };
+            double yb2 = 0.0, ybn2 = poll_block2(0);
+            const unsigned g2 = 8u * (unsigned)(2 * R + 1);   // byte offset of the line-2 coefficients
             const unsigned jl0 = (unsigned)(lane + R) & 31;   // j = (jl0 - i) & 31 at step i of a block
 #ifdef LP_SWEEP_TRACE
             const long long gc0 = clock64();
@@ -416,6 +455,7 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                 stage(blk + 3);
                 wait_chunk(blk + 1);
                 yb = ybn;
+                yb2 = ybn2;
                 // the serial has consumed every slot this block will write
                 {
                     const int tl31 = u0 + 31 - R;
@@ -426,31 +466,108 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                     }
                 }
                 __syncwarp();
+                if (has_prev2) {
+                    // line -/+2 was produced a line earlier: check the whole block once
+                    while (__any_sync(0xffffffff, bits(yb2) == SWEEP_SENTINEL)) {
+                        const int ua = u0 + lane;
+                        if (bits(yb2) == SWEEP_SENTINEL) yb2 = ld_poll(prev2 + (FWD ? ua : Kr - 1 - ua));
+                    }
+                }
+                if (u0 >= R && u0 + 32 <= Kr) {
+                    // interior block: every arrival valid and every step publishes; no
+                    // bounds tests, addresses advance incrementally
+                    const unsigned RBg = BRING * gstr;
+                    unsigned rofs = (unsigned)((FWD ? u0 : Kr - 1 - u0) & (BRING - 1)) * gstr;
+                    unsigned jq = jl0;
+                    double ynx = __shfl_sync(0xffffffff, yb, 0);
+                    double y2n = __shfl_sync(0xffffffff, yb2, 0);
+                    double qn = (int)jq <= tw ? lds(grp0 + rofs + 8 * jq) : 0.0;
+                    double q2n = (has_prev2 && (int)jq <= tw) ? lds(grp0 + rofs + g2 + 8 * jq) : 0.0;
+                    const unsigned tb = (unsigned)(u0 - R);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        if (i == 16) {
+                            ybn = poll_block(u0 + 32);
+                            ybn2 = poll_block2(u0 + 32);
+                        }
+                        const double acc2 = fma(q2n, y2n, acc);
+                        const double q = qn;
+                        double yn = ynx;
+                        if (i < 31) {
+                            ynx = __shfl_sync(0xffffffff, yb, i + 1);
+                            y2n = __shfl_sync(0xffffffff, yb2, i + 1);
+                            rofs = FWD ? (rofs + gstr == RBg ? 0u : rofs + gstr) : (rofs == 0u ? RBg - gstr : rofs - gstr);
+                            jq = (jq - 1u) & 31u;
+                            const bool ok = (int)jq <= tw;
+                            qn = ok ? lds(grp0 + rofs + 8 * jq) : 0.0;
+                            q2n = (has_prev2 && ok) ? lds(grp0 + rofs + g2 + 8 * jq) : 0.0;
+                        }
+                        while (bits(yn) == SWEEP_SENTINEL) {
+                            const int ua = u0 + lane;
+                            if (lane >= i) yb = pollv(FWD ? ua : Kr - 1 - ua);
+                            yn = __shfl_sync(0xffffffff, yb, i);
+                            if (i < 31) ynx = __shfl_sync(0xffffffff, yb, i + 1);
+#ifdef LP_SWEEP_TRACE
+                            ++nrepoll;
+#endif
+                        }
+                        acc = fma(q, yn, acc2);
+                        if (lane == ((i - R) & 31)) {
+                            sts_v(d0 + ((tb + (unsigned)i) & (RING - 1)) * 8, acc);
+                            acc = 0.0;
+                        }
+                    }
+                    continue;
+                }
+                // operands of step i are fetched during step i-1, off the arrival path
+                auto qaddr = [&](int i) -> unsigned {
+                    const int uarr = u0 + i;
+                    const int x = FWD ? uarr : Kr - 1 - uarr;
+                    const unsigned j = (jl0 - (unsigned)i) & 31;
+                    return grp0 + (unsigned)(x & (BRING - 1)) * gstr + 8 * j;
+                };
+                auto jok = [&](int i) { return (int)((jl0 - (unsigned)i) & 31) <= tw; };
                 double ynx = __shfl_sync(0xffffffff, yb, 0);
+                double y2n = __shfl_sync(0xffffffff, yb2, 0);
+                double qn = (u0 < Kr && jok(0)) ? lds(qaddr(0)) : 0.0;
+                double q2n = (has_prev2 && u0 < Kr && jok(0)) ? lds(qaddr(0) + g2) : 0.0;
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                     const int uarr = u0 + i, t = uarr - R;
-                    if (i == 16) ybn = poll_block(u0 + 32);
+                    if (i == 16) {
+                        ybn = poll_block(u0 + 32);
+                        ybn2 = poll_block2(u0 + 32);
+                    }
                     if (uarr < Kr) {
+                        const double acc2 = fma(q2n, y2n, acc);
+                        const double q = qn;
                         double yn = ynx;
+                        if (i < 31) {
+                            const bool nok = uarr + 1 < Kr && jok(i + 1);
+                            ynx = __shfl_sync(0xffffffff, yb, i + 1);
+                            y2n = __shfl_sync(0xffffffff, yb2, i + 1);
+                            qn = nok ? lds(qaddr(i + 1)) : 0.0;
+                            q2n = (has_prev2 && nok) ? lds(qaddr(i + 1) + g2) : 0.0;
+                        }
                         while (bits(yn) == SWEEP_SENTINEL) {
                             // re-poll the rest of the window: one round trip brings in
                             // every value produced since the last poll
                             const int ua = u0 + lane;
-                            if (lane >= i && ua < Kr) yb = ld_poll(prev + (FWD ? ua : Kr - 1 - ua));
+                            if (lane >= i && ua < Kr) yb = pollv(FWD ? ua : Kr - 1 - ua);
                             yn = __shfl_sync(0xffffffff, yb, i);
+                            if (i < 31) ynx = __shfl_sync(0xffffffff, yb, i + 1);
 #ifdef LP_SWEEP_TRACE
                             ++nrepoll;
 #endif
                         }
 #ifdef LP_SWEEP_TRACE
                         if (lane == 0 && a.trace && t == K / 2) a.trace[(size_t)tl * 16 + 10] = gtime();
+                        if (lane == 0 && a.trace && t == K / 2 - 64) a.trace[(size_t)tl * 16 + 11] = clock64();
+                        if (lane == 0 && a.trace && t == K / 2) a.trace[(size_t)tl * 16 + 11] = clock64() - a.trace[(size_t)tl * 16 + 11];
+                        if (lane == 0 && a.trace && t == K / 2 - 64) a.trace[(size_t)tl * 16 + 12] = nrepoll;
+                        if (lane == 0 && a.trace && t == K / 2) a.trace[(size_t)tl * 16 + 12] = nrepoll - a.trace[(size_t)tl * 16 + 12];
 #endif
-                        const int x = FWD ? uarr : Kr - 1 - uarr;
-                        const unsigned j = (jl0 - (unsigned)i) & 31;
-                        const double q = (int)j <= tw ? lds(grp0 + (unsigned)(x & (BRING - 1)) * gstr + 8 * j) : 0.0;
-                        if (i < 31) ynx = __shfl_sync(0xffffffff, yb, i + 1);
-                        acc = fma(q, yn, acc);
+                        acc = fma(q, yn, acc2);
                     }
                     if (lane == ((i - R) & 31) && t >= 0 && t < Kr) {
                         sts_v(d0 + (unsigned)(t & (RING - 1)) * 8, acc);
@@ -459,10 +576,7 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                 }
             }
 #ifdef LP_SWEEP_TRACE
-            if (lane == 0 && a.trace) {
-                a.trace[(size_t)tl * 16 + 11] = clock64() - gc0;
-                a.trace[(size_t)tl * 16 + 12] = nrepoll;
-            }
+            (void)gc0;
 #endif
             chunk_base += nch;
         } else if ((warp & 3) >= 2) {
@@ -495,8 +609,8 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                 const unsigned full0 = smem_addr(s_pfull);
                 volatile unsigned *v_cons = s_pcons;
                 const int W = g.W, nslot = a.nslot, ww = a.pr_ww;
-                const int oy0 = FWD ? -r : 2;   // line offset of segment 0
-                const int depL = FWD ? (iy >= 2 ? L - 2 : -1) : (iy <= K - 3 ? L + 2 : -1);
+                const int oy0 = FWD ? -r : 3;   // line offset of segment 0
+                const int depL = FWD ? (iy >= 3 ? L - 3 : -1) : (iy <= K - 4 ? L + 3 : -1);
                 for (int st = pw; st < ns; st += NP) {
                     const unsigned gs = stage_base + st;
                     const unsigned slot = gs % NSTAGE;
@@ -630,10 +744,10 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
             // checks remain the guard).
             int dep1, dep2;
             if (FWD) {
-                dep1 = (g.d > 1 && iy > 1) ? L - 2 : -1;
+                dep1 = (g.d > 1 && iy > 2) ? L - 3 : -1;
                 dep2 = (g.d > 2 && iz > 0) ? min(iy + r, K - 1) + K * (iz - 1) : -1;
             } else {
-                dep1 = (g.d > 1 && iy < K - 2) ? L + 2 : -1;
+                dep1 = (g.d > 1 && iy < K - 3) ? L + 3 : -1;
                 dep2 = (g.d > 2 && iz < K - 1) ? max(iy - r, 0) + K * (iz + 1) : -1;
             }
             double va[CH], vb[CH];
@@ -728,9 +842,10 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
 //              the row j steps later on the same line (fwd: L(ix+j, ix); bwd:
 //              U(ix-j, ix) / U(ix-j, ix-j)), 0 beyond r or the line end; rd = fwd 1,
 //              bwd 1/U(ix, ix);
-//   [nq, nq + 2r + 1): the coefficients by which y(line L-/+1, x = ix) enters the rows
-//              of line L that are j = 0..2r steps after its arrival step
-//              (fwd: rows x-r+j, slot (r-j, -1); bwd: rows x+r-j, slot (j-r, +1)).
+//   group section [2 (2r+1)], for line offsets m = 1, 2: the coefficients by which
+//              y(line L-/+m, x = ix) enters the rows of line L that are j = 0..2r steps
+//              after its arrival step (fwd: rows x-r+j, slot (r-j, -m); bwd: rows
+//              x+r-j, slot (j-r, +m)).
 __global__ void band_kernel(Geom g, const double *__restrict__ lu, int nq, int gsz,
                             double *__restrict__ blo, double *__restrict__ bup,
                             double *__restrict__ rdg) {
@@ -760,12 +875,13 @@ __global__ void band_kernel(Geom g, const double *__restrict__ lu, int nq, int g
                 }
             }
         } else {
-            const int j = l - nq;
-            o = (size_t)g.n * nq + (size_t)i * gsz + j;
-            if (g.d > 1 && j < 2 * r + 1) {
+            const int jj = l - nq;
+            o = (size_t)g.n * nq + (size_t)i * gsz + jj;
+            const int line = jj / (2 * r + 1) + 1, j = jj % (2 * r + 1);   // line -/+1 or -/+2
+            if (g.d > 1 && line <= 2) {
                 const int ixf = ix - r + j, ixb = ix + r - j;
-                if (ixf >= 0 && ixf < K) lo = lu[(size_t)(row0 + ixf) * g.S + g.c - g.W + r - j];
-                if (ixb >= 0 && ixb < K) up = lu[(size_t)(row0 + ixb) * g.S + g.c + g.W + j - r];
+                if (ixf >= 0 && ixf < K) lo = lu[(size_t)(row0 + ixf) * g.S + g.c - line * g.W + r - j];
+                if (ixb >= 0 && ixb < K) up = lu[(size_t)(row0 + ixb) * g.S + g.c + line * g.W + j - r];
             }
         }
         blo[o] = lo;
@@ -793,26 +909,71 @@ int prefill(int64_t n, double *a, double *b, cudaStream_t st) {
 }
 
 int band_nq(const Geom &g) { return g.r <= 7 ? 8 : 16; }
-int band_gsz(const Geom &g) { return g.d > 1 ? (int)round_up(2 * g.r + 1, 2) : 0; }
+int band_gsz(const Geom &g) { return g.d > 1 ? (int)round_up(2 * (2 * g.r + 1), 2) : 0; }
 int band_stride(const Geom &g) { return band_nq(g) + band_gsz(g); }
 
+#ifndef LP_SWEEP_CLUSTER
+#define LP_SWEEP_CLUSTER 4
+#endif
+
 template <bool FWD, int CH, int NQ>
-int run_sweep(const SweepArgs &a, const Geom &g, size_t smem, cudaStream_t st) {
+int run_sweep(SweepArgs a, const Geom &g, size_t smem, cudaStream_t st) {
     constexpr int NW = 16;
-    static int nblocks = 0;
+    static int nblocks = 0, csize = 1;
     static size_t smem_set = 0;
     auto kern = box_sweep_kernel<FWD, NW, CH, NQ>;
-    if (smem_set < smem) {
+    if (smem_set != smem) {
         LP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        LP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         int occ = 1, dev = 0, nsm = 148;
         LP_CUDA(cudaGetDevice(&dev));
         LP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * NW, smem));
         nblocks = occ * nsm;
+        csize = 1;
+        // clusters of LP_SWEEP_CLUSTER CTAs when every CTA can be resident
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = LP_SWEEP_CLUSTER;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(LP_SWEEP_CLUSTER, 1, 1);
+        cfg.blockDim = dim3(32 * NW, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (LP_SWEEP_CLUSTER > 1 && g.K <= 2048 &&
+            cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) == cudaSuccess && ncl > 0) {
+            csize = LP_SWEEP_CLUSTER;
+            nblocks = ncl * LP_SWEEP_CLUSTER;
+        }
+        cudaGetLastError();
         smem_set = smem;
     }
-    const int blocks = g.nlines < nblocks ? g.nlines : nblocks;
-    kern<<<blocks, 32 * NW, smem, st>>>(a);
+    a.csize = csize;
+    int blocks = nblocks;
+    if (csize == 1 && blocks > g.nlines) blocks = g.nlines;
+    if (csize > 1) {
+        const int need = (g.nlines + csize - 1) / csize * csize;
+        if (blocks > need) blocks = need;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = csize;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(blocks, 1, 1);
+        cfg.blockDim = dim3(32 * NW, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        LP_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    } else {
+        kern<<<blocks, 32 * NW, smem, st>>>(a);
+    }
     count_launch();
     LP_CHECK_LAUNCH();
     return LP_OK;
@@ -839,8 +1000,8 @@ int launch_sweep(lp_ilu *m, const double *rhs, double *out, cudaStream_t st) {
     const int nq = band_nq(g);
     a.gsz = band_gsz(g);
     a.band_g = a.band + (size_t)g.n * nq;
-    // producers: everything except the in-line entries and (d >= 2) line -/+1
-    const int excl = g.d > 1 ? g.W + g.r : g.r;
+    // producers: everything except the in-line entries and (d >= 2) lines -/+1, -/+2
+    const int excl = g.d > 1 ? 2 * g.W + g.r : g.r;
     a.lo = FWD ? 0 : g.c + excl + 1;
     a.nslot = FWD ? g.c - excl : g.S - (g.c + excl + 1);
     a.trace = nullptr;
@@ -862,12 +1023,16 @@ int launch_sweep(lp_ilu *m, const double *rhs, double *out, cudaStream_t st) {
     size_t smem = (size_t)BRING * (nq + a.gsz) * sizeof(double) + (size_t)a.nslot * (sizeof(int) + 4);
     smem = (size_t)round_up((int64_t)smem, 16);
     a.pr_ofs = (unsigned)smem;
-    a.nseg = g.d == 2 ? g.r - 1 : 0;
+    a.nseg = g.d == 2 ? g.r - 2 : 0;
     a.pr_rs = (int)round_up(a.nslot + 1, 2);
     a.pr_ww = (int)round_up(PR + 2 * g.r, 2);
     if (g.d == 2)
         smem += (size_t)NSTAGE * (PR * a.pr_rs + a.nseg * a.pr_ww) * sizeof(double) +
                 (size_t)a.nslot * sizeof(int);
+    smem = (size_t)round_up((int64_t)smem, 16);
+    a.yr_ofs = (unsigned)smem;
+    a.csize = 1;
+    if (g.K <= 2048) smem += (size_t)g.K * sizeof(double);   // line handoff buffer (clusters)
     smem += 16;
     LP_ARG(smem <= 227 * 1024, "sweep needs %zu bytes of shared memory (reach %d)", smem, g.r);
     LP_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(int), st));

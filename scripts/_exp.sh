@@ -1,2 +1,2 @@
 cd /root/repo
-LP_LIB_PATH=build/variants/itrace.so timeout 300 python scripts/trace_ilu.py cfg2 > gpurun_out/exp.txt 2>&1
+LP_LIB_PATH=build/variants/trace.so timeout 300 python scripts/trace_sweep.py cfg2 2>&1 | grep -E "detect|slope|second-half|group:" > gpurun_out/exp.txt

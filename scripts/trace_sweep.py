@@ -63,3 +63,5 @@ slope = (t[:, 3] - t[:, 2]) / half * 1e3
 print("per-line slope ns/step (lines 0..15):", " ".join(f"{v:.0f}" for v in slope[:16]))
 print("per-line detect latency us (lines 1..15):", " ".join(f"{v:.2f}" for v in lam[:15]))
 print("slope ns/step at lines 50,100,150,200,250:", " ".join(f"{slope[i]:.0f}" for i in (50, 100, 150, 200, 250) if i < nl))
+print("group: cycles per step over the 64 steps before mid (median over lines 1..)", np.median(tc[1:, 11] / 64.0),
+      "| re-polls in that window: median", np.median(tc[1:, 12]))
