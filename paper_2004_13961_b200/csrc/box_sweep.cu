@@ -30,6 +30,8 @@
 // lines in reverse, scaling by 1/U_tt).
 #include <math.h>
 
+#include <type_traits>
+
 #include "box_geom.cuh"
 #include "ilu.cuh"
 #include "smem_tma.cuh"
@@ -309,7 +311,10 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
 #ifdef LP_SWEEP_TRACE
             long long nspin_c = 0, nspin_a = 0;
 #endif
-            auto step = [&](const int t) {
+            // HP: the line has a previous line (A_t from the group); a compile-time
+            // flag so the step carries no branch on it
+            auto step = [&](const int t, auto HP) {
+                constexpr bool hp = decltype(HP)::value;
                 const double q = qn, e1c = e1n, rd = rdn, spt = spn;
                 double c = cn, av = dn;
 #ifdef LP_EXP_ALONE
@@ -319,18 +324,18 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                 const unsigned long long sb = bits(ring_sent(t));
 #ifdef LP_SWEEP_TRACE
                 while (bits(c) == sb) { c = lds_v(c0 + doff); ++nspin_c; }
-                if (has_prev)
+                if (hp)
                     while (bits(av) == sb) { av = lds_v(d0 + doff); ++nspin_a; }
 #else
                 while (bits(c) == sb) c = lds_v(c0 + doff);
-                if (has_prev)
+                if (hp)
                     while (bits(av) == sb) av = lds_v(d0 + doff);
 #endif
 #endif
-                const double y = fma(-e1, yprev, fma(rd, c - av, -spt));
+                const double y = fma(-e1, yprev, fma(rd, hp ? c - av : c, -spt));
                 // every lane stores the same values (no divergent branch)
                 sts_v(c0 + doff, ring_sent(t + RING));
-                if (has_prev) sts_v(d0 + doff, ring_sent(t + RING));
+                if (hp) sts_v(d0 + doff, ring_sent(t + RING));
 #ifdef LP_EXP_NOSTORE
                 if (t == Kr - 1)
 #endif
@@ -339,15 +344,16 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                 outp += ostep;
                 doff = (doff + 8) & (RING * 8 - 1);
                 cn = lds_v(c0 + doff);
-                if (has_prev) dn = lds_v(d0 + doff);
+                if (hp) dn = lds_v(d0 + doff);
                 roff = (roff + rstep) & (RB - 1);
                 qoff = (qoff - 8) & 255;
                 const unsigned rowa = in0 + roff;
                 lds2(rowa, e1n, rdn);
                 qn = (qoff - 16 < (NQ - 2) * 8) ? lds(rowa + qoff) : 0.0;
-                sp = ((unsigned)lane == ((unsigned)t & 31)) ? 0.0 : fma(q, y, sp);
-                // broadcast row t+1's finished sum (lane t+1 took no update this step)
+                // row t+1's finished sum: lane t+1 takes no update this step, so it is
+                // broadcast before the update, off the y_t -> y_{t+1} chain
                 spn = __shfl_sync(0xffffffff, sp, (t + 1) & 31);
+                sp = ((unsigned)lane == ((unsigned)t & 31)) ? 0.0 : fma(q, y, sp);
                 e1 = e1c;
                 yprev = y;
             };
@@ -371,12 +377,16 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                     for (int t = 32 * c; t < t1; ++t) {
                         if (t == th) mark(2);
                         if (t == th2 && lane == 0 && a.trace) a.trace[(size_t)tl * 16 + 15] = gtime();
-                        step(t);
+                        if (has_prev) step(t, std::true_type{});
+                        else step(t, std::false_type{});
                     }
                     continue;
                 }
 #endif
-                for (int t = 32 * c; t < t1; ++t) step(t);
+                if (has_prev)
+                    for (int t = 32 * c; t < t1; ++t) step(t, std::true_type{});
+                else
+                    for (int t = 32 * c; t < t1; ++t) step(t, std::false_type{});
             }
 #ifdef LP_SWEEP_TRACE
             mark(3);
