@@ -60,4 +60,5 @@ int box_build_bands(lp_ilu *m, cudaStream_t st);
 int box_apply(lp_ilu *m, const double *r, double *z, cudaStream_t st);
 int box_ilu0_2d_tasks(lp_ilu *m, double tol, unsigned long long *key, const unsigned char *full,
                       int *edone, cudaStream_t st);
+int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_t st);
 }  // namespace lp

@@ -530,6 +530,11 @@ int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st) {
         dfree(full);
         dfree(edone);
     }
+    if (g.d == 3 && b.mask) {
+        // row-per-CTA kernel (ilu_box3d.cu)
+        const int rt = box_ilu0_3d_rows(m, tol, key, st);
+        if (rt == LP_OK) done = true;
+    }
     if (done) {
     } else if (g.d <= 2 && !window_ok && g.r + 1 <= LNW && line_smem <= 220 * 1024) {
         LP_CUDA(cudaFuncSetAttribute(box_ilu0_line_kernel<LNW>,

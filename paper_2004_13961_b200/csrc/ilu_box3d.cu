@@ -1,0 +1,411 @@
+// ILU(0) of a 3-D box matrix: one CTA per row, the row resident in registers.
+//
+// IKJ elimination (sparse.py:116-139) of row i = (x, y, z) visits its lower
+// slots in column order: pivot planes pz = -r..0, pivot lines py, x fastest,
+// the in-line pivots x-r..x-1 last.  The targets of pivot p = (px, py, pz) are
+// the offsets t > p of the box with t - p in the box:
+//
+//     tz in [pz, pz + r],  |tx - px| <= r,  |ty - py| <= r,
+//
+// and the pivot-row entry of target t is slot t - s_p + c (offsets subtract
+// slot-linearly).  A 3-D row has (2r+1)^3 slots (9,261 at r = 10), so one row
+// is one CTA's working set: thread q = (ty, tx) owns the column of 2r+1
+// entries (all tz) in registers; a pivot step is
+//
+//   owner of slot p:  l = v[pz] / u_kk, v[pz] = l, broadcast l (shared, 1 barrier)
+//   every thread:     v[pz + j] -= l * u_k[t - s_p + c],  j = 0..r (its active planes)
+//
+// with pz a compile-time constant inside the unrolled plane loop, so the
+// register file is indexed statically.  The pivot-row entries of the next D
+// pivots are staged by per-thread cp.async copies into a shared ring (each
+// thread reads only what it copied itself, so the ring needs no barrier).
+// Every entry receives its updates in the reference's k order, each a
+// separately rounded multiply and subtract: the factors are the reference's
+// bit for bit.
+//
+// Rows are taken in natural order by an atomic ticket; a row only waits on
+// smaller rows, which are resident or done, so the grid cannot deadlock.
+// Completion is published per x-line as a contiguous row prefix
+// (flags[line] = rows done): one acquire poll per pivot line (per pivot for the
+// in-line ones); rows of a line finish in order because row x eliminates x - 1 last.
+#include <math.h>
+
+#include "box_geom.cuh"
+#include "ilu.cuh"
+
+namespace lp {
+
+extern unsigned long long *g_ilu_trace;
+extern size_t g_ilu_trace_n;
+
+namespace {
+
+template <int R>
+struct Cfg {
+    static constexpr int W = 2 * R + 1;
+    static constexpr int W2 = W * W;
+    static constexpr int S = W2 * W;
+    static constexpr int C = (S - 1) / 2;
+    static constexpr int TPB = (W2 + 31) / 32 * 32;     // one thread per (tx, ty) column
+    static constexpr int STAGE = (R + 1) * TPB;         // doubles per staged pivot
+    static constexpr int D = STAGE * 8 * 5 <= 200 * 1024 ? 5 : 4;   // pivots in flight (r <= 10: 5)
+};
+
+__device__ __forceinline__ int ld_acquire(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(int *p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void cp_async8(unsigned dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct Ilu3Args {
+    Geom g;
+    double *lu;
+    const uint32_t *mask;
+    int *lineflags;   // [nlines] rows of the line that are final
+    int *ticket;
+    double tol;
+    unsigned long long *bad;
+    unsigned long long *trace;   // LP_ILU_TRACE builds: [n][4] timestamps
+};
+
+__device__ __forceinline__ unsigned long long gtime3() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ bool bit_of(const uint32_t *bits, int t) {
+    return (bits[t >> 5] >> (t & 31)) & 1u;
+}
+
+// First in-pattern slot in [from, end).
+__device__ __forceinline__ int next_slot(const uint32_t *bits, int from, int end) {
+    if (from >= end) return end;
+    int w = from >> 5;
+    uint32_t m = bits[w] & (0xFFFFFFFFu << (from & 31));
+    const int wlast = (end - 1) >> 5;
+    while (!m) {
+        if (++w > wlast) return end;
+        m = bits[w];
+    }
+    const int s = (w << 5) + __ffs(m) - 1;
+    return s < end ? s : end;
+}
+
+// IEEE quotient a / b from y = RN(1 / b) (Markstein: q0 = RN(a y) is within one
+// ulp, r = a - b q0 is exact, RN(q0 + r y) = RN(a / b)); with y computed ahead,
+// only three dependent operations remain on a pivot step's critical path.
+__device__ __forceinline__ double div_by_recip(double a, double b, double y) {
+    const double q0 = __dmul_rn(a, y);
+    const double r = __fma_rn(-b, q0, a);
+    return __fma_rn(r, y, q0);
+}
+
+template <int R>
+__global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __grid_constant__ Ilu3Args a) {
+    using G = Cfg<R>;
+    constexpr int W = G::W, W2 = G::W2, S = G::S, C = G::C, TPB = G::TPB, D = G::D;
+    static_assert(D >= 3, "the next pivot's data must land one step early");
+    extern __shared__ __align__(16) double sm[];
+    double *stage = sm;                                                 // [D][R+1][TPB]
+    double *spiv = stage + (size_t)D * G::STAGE;                        // [D]
+    uint32_t *bits = reinterpret_cast<uint32_t *>(spiv + D);            // [mw]
+    int *plist = reinterpret_cast<int *>(bits + a.g.mw);                // [C] packed pivots
+    __shared__ double sh_l[2];
+    __shared__ long long sh_i;
+    __shared__ int sh_wcount[(C + 31) / 32 + 1];
+    const int tid = threadIdx.x;
+    const bool col = tid < W2;
+    const int tx = col ? tid % W - R : 0, ty = col ? tid / W - R : 0;
+    const int K = a.g.K;
+    const int mw = a.g.mw;
+    const int64_t n = a.g.n;
+    const unsigned stage_s = (unsigned)__cvta_generic_to_shared(stage);
+    const unsigned spiv_s = (unsigned)__cvta_generic_to_shared(spiv);
+    constexpr int NWL = (C + 31) / 32;   // mask words of the lower half
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) sh_i = atomicAdd(a.ticket, 1);
+        __syncthreads();
+        const int64_t i = sh_i;
+        if (i >= n) return;
+        const int ix = (int)(i % K);
+        const int64_t L = i / K;
+#ifdef LP_ILU_TRACE
+        if (tid == 0) a.trace[i * 8] = gtime3();
+#endif
+        double *gi = a.lu + (size_t)i * S;
+        for (int q = tid; q < mw; q += TPB) bits[q] = a.mask[(size_t)i * mw + q];
+        double v[W];
+#pragma unroll
+        for (int z = 0; z < W; ++z) v[z] = col ? __ldcg(gi + tid + z * W2) : 0.0;
+        __syncthreads();
+        // pivot list: the in-pattern lower slots in order, packed
+        // s | (px + R) << 14 | (py + R) << 19 | (pz + R) << 24
+        for (int w = tid; w < NWL; w += TPB) {
+            uint32_t m = bits[w];
+            if (w == NWL - 1 && (C & 31)) m &= (1u << (C & 31)) - 1u;
+            sh_wcount[w] = __popc(m);
+        }
+        __syncthreads();
+        if (tid < 32) {
+            int run = 0;
+            for (int w0 = 0; w0 < NWL; w0 += 32) {
+                const int w = w0 + tid;
+                const int cnt = w < NWL ? sh_wcount[w] : 0;
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (tid >= o) incl += t;
+                }
+                if (w < NWL) sh_wcount[w] = run + incl - cnt;
+                run += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (tid == 0) sh_wcount[NWL] = run;
+        }
+        __syncthreads();
+        for (int w = tid; w < NWL; w += TPB) {
+            uint32_t m = bits[w];
+            if (w == NWL - 1 && (C & 31)) m &= (1u << (C & 31)) - 1u;
+            int o = sh_wcount[w];
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                const int s = w * 32 + b;
+                plist[o++] = s | ((s % W) << 14) | (((s / W) % W) << 19) | ((s / W2) << 24);
+            }
+        }
+        unsigned colbits = 0;
+        if (col) {
+#pragma unroll
+            for (int z = 0; z < W; ++z) colbits |= (unsigned)bit_of(bits, tid + z * W2) << z;
+        }
+        __syncthreads();
+        const int npiv = sh_wcount[NWL];
+
+        // ---- prefetch: stages pivot pn into ring slot pn % D
+        int pn = 0;
+        int ready_line = -1 << 20;
+#ifdef LP_ILU_TRACE
+        unsigned long long spin_in = 0, spin_line = 0;
+#endif
+        auto prefetch = [&]() {
+            if (pn < npiv) {
+                const int e = plist[pn];
+                const int ps = e & 0x3FFF;
+                const int px = ((e >> 14) & 31) - R, py = ((e >> 19) & 31) - R, pz = (e >> 24) - R;
+                const int64_t Lk = L + py + (int64_t)K * pz;
+                const int lid = pz * W + py;
+                if (lid == 0) {
+                    while (ld_acquire(a.lineflags + Lk) < ix + px + 1) {
+#ifdef LP_ILU_TRACE
+                        ++spin_in;
+#endif
+                    }
+                } else if (lid != ready_line) {
+                    const int need = min(K, ix + R + 1);
+                    while (ld_acquire(a.lineflags + Lk) < need) {
+#ifdef LP_ILU_TRACE
+                        ++spin_line;
+#endif
+                    }
+                    ready_line = lid;
+                }
+                const double *uk = a.lu + (size_t)(i + px + (int64_t)K * (py + (int64_t)K * pz)) * S;
+                const int slot = pn % D;
+                if (tid == (py + R) * W + (px + R)) cp_async8(spiv_s + slot * 8, uk + C);
+                if (col && abs(tx - px) <= R && abs(ty - py) <= R) {
+                    unsigned m = (colbits >> (pz + R)) & ((1u << (R + 1)) - 1u);
+                    if (!(ty > py || (ty == py && tx > px))) m &= ~1u;
+                    const double *src = uk + (C - ps) + tid + (pz + R) * W2;
+                    const unsigned dst = stage_s + (unsigned)((slot * (R + 1)) * TPB + tid) * 8;
+#pragma unroll
+                    for (int j = 0; j <= R; ++j)
+                        if ((m >> j) & 1u) cp_async8(dst + j * TPB * 8, src + j * W2);
+                }
+            }
+            cp_commit();
+            ++pn;
+        };
+#pragma unroll 1
+        for (int q = 0; q < D; ++q) prefetch();
+
+        // ---- pivot steps, plane by plane (pz static inside the unrolled loop).
+        // Step en: barrier; every thread applies l_en to its targets; the owner of
+        // the next pivot (same plane) then finishes that pivot's l at once, so the
+        // critical path of a step is barrier -> one update -> one division.
+        int en = 0;
+        bool have_l = false;   // l of pivot en already computed and published
+#pragma unroll
+        for (int pzi = 0; pzi <= R; ++pzi) {
+#pragma unroll 1
+            while (en < npiv) {
+                const int e = plist[en];
+                if ((e >> 24) != pzi) break;
+                const int px = ((e >> 14) & 31) - R, py = ((e >> 19) & 31) - R;
+                const int slot = en % D;
+                cp_wait<D - 2>();   // this pivot's and the next pivot's data have landed
+                if (!have_l && tid == (py + R) * W + (px + R)) {
+                    const double piv = spiv[slot];
+                    const double l = __ddiv_rn(v[pzi], piv);
+                    v[pzi] = l;
+                    sh_l[en & 1] = l;
+                    if (fabs(piv) < a.tol) {
+                        const int64_t k = i + px + (int64_t)K * (py + (int64_t)K * (pzi - R));
+                        atomicMin(a.bad, (unsigned long long)(i * n + k));
+                    }
+                }
+                // next pivot of this plane and its owner
+                const int e1 = en + 1 < npiv ? plist[en + 1] : -1;
+                const bool next_here = e1 >= 0 && (e1 >> 24) == pzi;
+                const int own1 = ((e1 >> 19) & 31) * W + ((e1 >> 14) & 31);
+                double y1 = 0.0, piv1 = 0.0;
+                if (next_here && tid == own1) {
+                    piv1 = spiv[(en + 1) % D];
+                    y1 = __drcp_rn(piv1);
+                }
+                __syncthreads();
+                const double l = sh_l[en & 1];
+                if (col && abs(tx - px) <= R && abs(ty - py) <= R) {
+                    unsigned m = (colbits >> pzi) & ((1u << (R + 1)) - 1u);
+                    if (!(ty > py || (ty == py && tx > px))) m &= ~1u;
+                    const double *src = stage + (size_t)slot * (R + 1) * TPB + tid;
+                    // the next pivot's entry (plane pzi, j = 0) first
+                    if (m & 1u) v[pzi] = __dsub_rn(v[pzi], __dmul_rn(l, src[0]));
+                    if (next_here && tid == own1) {
+                        const double l1 = div_by_recip(v[pzi], piv1, y1);
+                        v[pzi] = l1;
+                        sh_l[(en + 1) & 1] = l1;
+                        if (fabs(piv1) < a.tol) {
+                            const int px1 = ((e1 >> 14) & 31) - R, py1 = ((e1 >> 19) & 31) - R;
+                            const int64_t k = i + px1 + (int64_t)K * (py1 + (int64_t)K * (pzi - R));
+                            atomicMin(a.bad, (unsigned long long)(i * n + k));
+                        }
+                    }
+#pragma unroll
+                    for (int j = 1; j <= R; ++j)
+                        if (pzi + j < W && ((m >> j) & 1u))
+                            v[pzi + j] = __dsub_rn(v[pzi + j], __dmul_rn(l, src[j * TPB]));
+                } else if (next_here && tid == own1) {
+                    const double l1 = div_by_recip(v[pzi], piv1, y1);
+                    v[pzi] = l1;
+                    sh_l[(en + 1) & 1] = l1;
+                    if (fabs(piv1) < a.tol) {
+                        const int px1 = ((e1 >> 14) & 31) - R, py1 = ((e1 >> 19) & 31) - R;
+                        const int64_t k = i + px1 + (int64_t)K * (py1 + (int64_t)K * (pzi - R));
+                        atomicMin(a.bad, (unsigned long long)(i * n + k));
+                    }
+                }
+                have_l = next_here;
+                ++en;
+                prefetch();
+            }
+#ifdef LP_ILU_TRACE
+            if (pzi == R - 1 && tid == 0) a.trace[i * 8 + 1] = gtime3();
+#endif
+        }
+        cp_wait<0>();
+#ifdef LP_ILU_TRACE
+        if (tid == 0) a.trace[i * 8 + 2] = gtime3();
+#endif
+        if (col) {
+#pragma unroll
+            for (int z = 0; z < W; ++z) __stcg(gi + tid + z * W2, v[z]);
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            // publish the line's contiguous prefix (row x - 1 publishes first)
+            while (ld_acquire(a.lineflags + L) != ix) {
+            }
+            st_release(a.lineflags + L, ix + 1);
+#ifdef LP_ILU_TRACE
+            a.trace[i * 8 + 3] = gtime3();
+            a.trace[i * 8 + 4] = spin_line;
+            a.trace[i * 8 + 5] = spin_in;
+            a.trace[i * 8 + 6] = (unsigned long long)npiv;
+#endif
+        }
+    }
+}
+
+template <int R>
+int launch3(const Ilu3Args &a, cudaStream_t st) {
+    using G = Cfg<R>;
+    const size_t smem = ((size_t)G::D * G::STAGE + G::D) * sizeof(double) +
+                        (size_t)a.g.mw * sizeof(uint32_t) + (size_t)G::C * sizeof(int) + 16;
+    LP_CUDA(cudaFuncSetAttribute(box_ilu0_3d_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    int dev = 0, nsm = 148, occ = 1;
+    LP_CUDA(cudaGetDevice(&dev));
+    LP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, box_ilu0_3d_kernel<R>, G::TPB, smem));
+    if (occ < 1) return LP_ERR_ARG;
+    int64_t blocks = (int64_t)occ * nsm;
+    if (blocks > a.g.n) blocks = a.g.n;
+    box_ilu0_3d_kernel<R><<<(unsigned)blocks, G::TPB, smem, st>>>(a);
+    count_launch();
+    LP_CHECK_LAUNCH();
+    return LP_OK;
+}
+
+}  // namespace
+
+// Launches the 3-D row kernel; returns a negative code when it does not apply
+// (r outside 1..10), in which case the caller uses the generic kernel.
+int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_t st) {
+    BoxLayout &b = m->box;
+    Geom g = geom_of(b);
+    if (g.d != 3) return LP_ERR_ARG;
+    Ilu3Args a;
+    a.g = g;
+    a.lu = b.lu;
+    a.mask = b.mask;
+    a.lineflags = m->flags;
+    a.ticket = m->ticket;
+    a.tol = tol;
+    a.bad = key;
+    a.trace = nullptr;
+#ifdef LP_ILU_TRACE
+    {
+        static unsigned long long *tr = nullptr;
+        static size_t trn = 0;
+        if (trn < (size_t)g.n * 8) {
+            if (tr) dfree(tr);
+            trn = (size_t)g.n * 8;
+            dalloc(&tr, trn, "ilu trace");
+        }
+        cudaMemsetAsync(tr, 0, trn * 8, st);
+        a.trace = tr;
+        g_ilu_trace = tr;
+        g_ilu_trace_n = trn;
+    }
+#endif
+    switch (g.r) {
+        case 1: return launch3<1>(a, st);
+        case 2: return launch3<2>(a, st);
+        case 3: return launch3<3>(a, st);
+        case 4: return launch3<4>(a, st);
+        case 5: return launch3<5>(a, st);
+        case 6: return launch3<6>(a, st);
+        case 7: return launch3<7>(a, st);
+        case 8: return launch3<8>(a, st);
+        case 9: return launch3<9>(a, st);
+        case 10: return launch3<10>(a, st);
+        default: return LP_ERR_ARG;
+    }
+}
+
+}  // namespace lp

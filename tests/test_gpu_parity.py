@@ -197,6 +197,21 @@ def test_ilu0_csr_bitwise(golden, name, N, T):
     assert relerr(precond_apply(f, g[k + "_r"]), g[k + "_z"]) < 1e-13
 
 
+@pytest.mark.parametrize("name,N,T", [("cfg4", 12, 8), ("cfg5", 12, 3), ("cfg4", 16, 4),
+                                      ("cfg5", 20, 2), ("cfg4", 9, 1), ("cfg2", 20, 10)])
+def test_box_factors_bitwise_vs_csr(name, N, T):
+    """The box-layout factorisation (3-D: row-per-CTA kernel; 2-D: task graph)
+    equals, bit for bit, the CSR kernel on the same M -- which reproduces the
+    reference's factors bit for bit (test_ilu0_csr_bitwise)."""
+    w = wl.CONFIGS[name]()
+    m = assemble_M(spec_of(w, N), T, T)
+    csr = SparseMatrix(m.n, m.indptr, m.indices, m.values)
+    fb, fc = ilu0(m), ilu0(csr)
+    assert sha(fb.L.indptr, fb.L.indices) == sha(fc.L.indptr, fc.L.indices)
+    assert sha(fb.L.values) == sha(fc.L.values)
+    assert sha(fb.U.values) == sha(fc.U.values)
+
+
 def test_sparse_known_answers():
     # reference tests/test_sparse.py:144-160
     d = np.array([[1.0, 0, 0], [0.5, 1.0, 0], [0, 0.5, 1.0]])
