@@ -999,6 +999,11 @@ int launch_nq(const SweepArgs &a, const Geom &g, size_t smem, cudaStream_t st) {
 template <bool FWD>
 int launch_sweep(lp_ilu *m, const double *rhs, double *out, cudaStream_t st) {
     Geom g = geom_of(m->box);
+    if (box_sweep3d_applies(g)) {
+        int *tk = m->ticket + (FWD ? 0 : 1);
+        LP_CUDA(cudaMemsetAsync(tk, 0, sizeof(int), st));
+        return box_sweep3d(m, FWD, rhs, out, tk, st);
+    }
     LP_ARG(g.r <= 15, "stencil reach %d > 15 is not supported by the sweep kernel", g.r);
     SweepArgs a;
     a.g = g;
@@ -1054,6 +1059,7 @@ int launch_sweep(lp_ilu *m, const double *rhs, double *out, cudaStream_t st) {
 int box_build_bands(lp_ilu *m, cudaStream_t st) {
     BoxLayout &b = m->box;
     Geom g = geom_of(b);
+    if (box_sweep3d_applies(g)) return LP_OK;   // the 3-D sweeps read the factors directly
     const int bs = band_stride(g);
     int rc;
     if (!b.band_lo && ((rc = dalloc(&b.band_lo, (size_t)b.n * bs, "band")) ||

@@ -1,0 +1,471 @@
+// ILU(0) forward / backward sweeps of a 3-D box matrix (forward_sub /
+// backward_sub, sparse.py:175-216) as a bandwidth-first line wavefront.
+//
+// In 3-D a row carries (2r+1)^3 / 2 factor entries (4,630 at r = 10, 37 KB), so
+// a sweep streams ~67 GB at cfg 4 while its dependency chain is short
+// (16,759 levels, 0.6 us per level at the HBM roofline).  The
+// kernel is therefore built around the factor stream:
+//
+//  * a CTA owns one x-line at a time (lines by atomic ticket in sweep order, so
+//    it only waits on lines held by running CTAs);
+//  * a loader lane streams the line's rows, each row's lower (forward) or
+//    diagonal+upper (backward) half one contiguous TMA bulk copy, into a ring
+//    of shared-memory row buffers (full / empty mbarriers);
+//  * producer thread q owns source line q of the stencil (the r (2r+1) + r
+//    off-line slot lines): it keeps the 2r+1 values y(src, x-r..x+r) it needs
+//    in a register window that slides by one value per row (loads issued P rows
+//    ahead, polled only if they came back as the sentinel), and contributes
+//    sum_ox L(x; q, ox) y(src, x+ox); warp sums go to a shared ring;
+//  * the serial warp adds the warp sums and runs the in-line recurrence
+//    y_x = rhs_x - C_x - sum_d L(x, x-d) y_{x-d}  (backward: z_x = (...)/U_xx)
+//    and publishes y_x.
+//
+// Synchronisation is fence-free as in box_sweep.cu: the output is pre-filled
+// with a NaN sentinel and every value is its own flag (aligned 64-bit
+// accesses are single-copy atomic; relaxed .gpu loads), computed NaNs are
+// canonicalised.  The backward sweep is the mirror image (lines and rows in
+// reverse, the upper half of each row, division by the diagonal).
+#include <math.h>
+
+#include "box_geom.cuh"
+#include "ilu.cuh"
+#include "smem_tma.cuh"
+
+namespace lp {
+
+extern unsigned long long *g_trace;   // LP_SWEEP_TRACE builds (box_sweep.cu)
+extern size_t g_trace_n;
+
+namespace {
+
+__device__ __forceinline__ unsigned long long gtime_dep(double dep) {
+    unsigned long long t;
+    asm volatile("{ .reg .f64 d; mov.f64 d, %1; mov.u64 %0, %%globaltimer; }" : "=l"(t) : "d"(dep));
+    return t;
+}
+
+__device__ __forceinline__ unsigned long long gtime_s3() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+constexpr unsigned long long SENT3 = 0xFFF4C0FFEE5EED00ull;   // = SWEEP_SENTINEL (box_sweep.cu)
+constexpr int RRED = 16;   // rows of warp sums in flight
+
+template <int R>
+struct S3 {
+    static constexpr int W = 2 * R + 1;
+    static constexpr int W2 = W * W;
+    static constexpr int S = W2 * W;
+    static constexpr int C = (S - 1) / 2;
+    static constexpr int NQ = R * W + R;                  // off-line slot lines per side
+    static constexpr int NPW = (NQ + 31) / 32;            // producer warps
+    static constexpr int NT = 32 * (NPW + 2);             // + serial warp + loader warp
+    static constexpr int ROWD = (C + 1 + 1 + 1) / 2 * 2;  // staged doubles per row (+ alignment shift)
+#ifdef LP_S3_NR
+    static constexpr int NR = LP_S3_NR;
+#else
+    static constexpr int NR = (190 * 1024) / (ROWD * 8) < 6 ? (190 * 1024) / (ROWD * 8) : 6;
+#endif
+    // rows of look-ahead of the window loads (P) and of their re-polls (PR); both
+    // divide W (static register rotation)
+#ifdef LP_S3_P
+    static constexpr int P = LP_S3_P;
+    static constexpr int PR = LP_S3_PR;
+#else
+    static constexpr int P = W % 7 == 0 ? 7 : W;
+    static constexpr int PR = 1;   // measured (cfg-4 recipe, N=64): 1 row 17.9 ms, 3 rows 22.0 ms per pair
+#endif
+};
+
+struct Sweep3Args {
+    Geom g;
+    const double *lu;
+    const double *rhs;
+    double *out;
+    int *ticket;
+    unsigned long long *trace;   // LP_SWEEP_TRACE: [nlines][8] (ticket time, rows 0 / K/4 / K/2 / K-1 done)
+};
+
+__device__ __forceinline__ double ld_rel(const double *p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Weak L2 load for the look-ahead reads: a strong (.relaxed.gpu) load holds
+// back the warp's following shared-memory loads until it completes (measured:
+// one L2 round trip per row), while a value read too early is only re-polled.
+__device__ __forceinline__ double ld_l2(const double *p, unsigned long long pol) {
+    double v;
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+// Published values stay in L2 (evict_last) while the factor stream passes
+// through it (evict_first): a consumer's poll must not queue behind the
+// stream's HBM traffic.
+__device__ __forceinline__ void st_keep(double *p, double v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ bool is_sent(double v) {
+    return (unsigned long long)__double_as_longlong(v) == SENT3;
+}
+
+__device__ __forceinline__ double canon3(double v) {
+    return isnan(v) ? __longlong_as_double(0x7FF8000000000000ll) : v;
+}
+
+__device__ __forceinline__ double wait_value(const double *p, double v) {
+    while (is_sent(v)) v = ld_rel(p);
+    return v;
+}
+
+template <bool FWD, int R>
+__global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_constant__ Sweep3Args a) {
+    using G = S3<R>;
+    constexpr int W = G::W, S = G::S, C = G::C, NQ = G::NQ, NPW = G::NPW, ROWD = G::ROWD, NR = G::NR;
+    constexpr int P3 = G::P, PR3 = G::PR;
+    extern __shared__ __align__(16) double ring[];                         // [NR][ROWD], rhs [K]
+    __shared__ __align__(8) unsigned long long mbar[NR];                    // full[NR]
+    __shared__ double red[RRED][NPW];
+    __shared__ int sh_line;
+    __shared__ int rowready[NR];   // row (CTA step) whose TMA copy has landed in the slot
+    __shared__ int slotdone[NR];   // consumers done with the slot, cumulative
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int K = a.g.K;
+    const int nlines = a.g.nlines;
+    const unsigned ring_s = smem_addr(ring);
+    double *rhs_s = ring + NR * ROWD;
+    const unsigned full_s = smem_addr(mbar);
+    if (tid == 0) {
+        for (int q = 0; q < NR; ++q) mbar_init(full_s + q * 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int q = tid; q < NR; q += blockDim.x) {
+        rowready[q] = -1;
+        slotdone[q] = 0;
+    }
+    for (int q = tid; q < RRED * NPW; q += blockDim.x)
+        (&red[0][0])[q] = __longlong_as_double((long long)SENT3);
+    __syncthreads();
+    const unsigned red_s = smem_addr(&red[0][0]);
+    // Consumers never touch an mbarrier: an mbarrier wait or arrive in a warp
+    // with outstanding global loads waits for those loads (measured: one L2
+    // round trip per row).  A watcher lane turns each TMA completion into a
+    // shared flag, and consumers count themselves off a slot with a shared atomic.
+    auto wait_row = [&](int slot, long long gs) {
+        const unsigned fa = smem_addr(&rowready[slot]);
+        int f;
+        do {
+            asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(f) : "r"(fa) : "memory");
+        } while (f != (int)gs);
+    };
+
+    // region of a row staged per step: forward slots [0, C), backward [C, S)
+    constexpr int base = FWD ? 0 : C;
+    constexpr int len = FWD ? C : C + 1;
+    long long gstep = 0;   // rows processed by this CTA (mbarrier phases run across lines)
+    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    for (;;) {
+        if (tid == 64) sh_line = atomicAdd(a.ticket, 1);
+        __syncthreads();
+        const int t = sh_line;
+        __syncthreads();
+        if (t >= nlines) return;
+        const int L = FWD ? t : nlines - 1 - t;
+        const int ly = L % K, lz = L / K;
+        const int64_t row0 = (int64_t)L * K;
+#ifdef LP_SWEEP_TRACE
+        if (tid == 0) a.trace[(size_t)t * 8] = gtime_s3();
+#endif
+
+        if (warp == 0) {
+            // ---------------- loader lane
+            if (lane == 0) {
+                for (int u = 0; u < K; ++u) {
+                    const long long gs = gstep + u;
+                    const int slot = (int)(gs % NR);
+                    if (gs >= NR) {
+                        // all NPW + 1 consumers of the slot's previous row are done
+                        const int need = (int)(gs / NR) * (NPW + 1);
+                        const unsigned ca = smem_addr(&slotdone[slot]);
+                        int f;
+                        for (;;) {
+                            asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(f) : "r"(ca) : "memory");
+                            if (f >= need) break;
+                            __nanosleep(32);
+                        }
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    }
+                    const int x = FWD ? u : K - 1 - u;
+                    const int64_t e0 = (row0 + x) * S + base;
+                    const int64_t ea = e0 & ~(int64_t)1;
+                    const unsigned bytes = (unsigned)(((e0 - ea) + len + 1) / 2 * 2) * 8;
+                    mbar_expect(full_s + slot * 8, bytes);
+                    bulk_g2s_hint(ring_s + (unsigned)slot * ROWD * 8, a.lu + ea, bytes, full_s + slot * 8, pol_stream);
+#ifdef LP_SWEEP_TRACE
+                    if ((t == 0 || t == nlines / 2) && u < 32)
+                        a.trace[(size_t)nlines * 8 + (t ? 128 : 0) + u * 4] = gtime_s3();
+#endif
+                }
+            }
+            else if (lane == 1) {
+                // watcher: turns each row's TMA completion into a shared flag, so the
+                // producer warps (which hold outstanding global loads) never execute
+                // an mbarrier wait
+                for (int u = 0; u < K; ++u) {
+                    const long long gs = gstep + u;
+                    const int slot = (int)(gs % NR);
+                    mbar_wait(full_s + slot * 8, (unsigned)((gs / NR) & 1));
+                    asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(smem_addr(&rowready[slot])), "r"((int)gs) : "memory");
+                }
+            }
+        } else if (warp == 1) {
+            // ---------------- serial warp: in-line recurrence (lane 0)
+            // the line's right-hand side, one coalesced pass into shared memory
+            for (int x = lane; x < K; x += 32) rhs_s[x] = __ldcg(a.rhs + row0 + x);
+            __syncwarp();
+            if (lane == 0) {
+                double h[R];   // h[d-1] = output of the row d steps back in processing order
+#pragma unroll
+                for (int d = 0; d < R; ++d) h[d] = 0.0;
+                for (int u = 0; u < K; ++u) {
+                    const long long gs = gstep + u;
+                    const int slot = (int)(gs % NR);
+                    const int x = FWD ? u : K - 1 - u;
+                    const int64_t i = row0 + x;
+                    const double rhs = rhs_s[x];
+                    wait_row(slot, gs);
+                    const int sh = (int)(((i * S + base) & 1));
+                    const unsigned rowa = ring_s + (unsigned)(slot * ROWD + sh) * 8;
+#ifdef LP_SWEEP_TRACE
+                    if (t == 1 && u < 64) a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 0] = gtime_s3();
+#endif
+                    // in-line coefficients: forward L(x, x-d) at slot C-d; backward U(x, x+d) at C+d
+                    double acc = rhs;
+#pragma unroll
+                    for (int d = R; d >= 2; --d) {
+                        const bool ok = FWD ? x - d >= 0 : x + d < K;
+                        const double cf = lds(rowa + (unsigned)(FWD ? C - d : d) * 8);
+                        if (ok) acc = __fma_rn(-cf, h[d - 1], acc);
+                    }
+                    const double c1 = lds(rowa + (unsigned)(FWD ? C - 1 : 1) * 8);
+                    const double diag = FWD ? 1.0 : lds(rowa);
+                    atomicAdd(&slotdone[slot], 1);
+                    // warp sums of the producers
+                    const int rr = (int)(gs % RRED);
+                    double csum = 0.0;
+#pragma unroll
+                    for (int w = NPW - 1; w >= 0; --w) {
+                        const unsigned ra = red_s + (unsigned)(rr * NPW + w) * 8;
+                        double v = lds_v(ra);
+                        while (is_sent(v)) v = lds_v(ra);
+                        sts_v(ra, __longlong_as_double((long long)SENT3));
+                        csum += v;
+                    }
+                    acc -= csum;
+#ifdef LP_SWEEP_TRACE
+                    if (t == 1 && u < 64) a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 1] = gtime_dep(acc);
+#endif
+                    if (FWD ? x >= 1 : x + 1 < K) acc = __fma_rn(-c1, h[0], acc);
+                    const double y = canon3(FWD ? acc : __ddiv_rn(acc, diag));
+                    st_keep(a.out + i, y, pol_keep);
+#ifdef LP_SWEEP_TRACE
+                    if (t == 1 && u < 64) a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 2] = gtime_s3();
+#endif
+#ifdef LP_SWEEP_TRACE
+                    if ((t == 0 || t == nlines / 2) && u < 32)
+                        a.trace[(size_t)nlines * 8 + (t ? 128 : 0) + u * 4 + 3] = gtime_s3();
+                    if (u == 0 || u == K / 4 || u == K / 2 || u == K - 1)
+                        a.trace[(size_t)t * 8 + 1 + (u == 0 ? 0 : u == K / 4 ? 1 : u == K / 2 ? 2 : 3)] = gtime_s3();
+#endif
+#pragma unroll
+                    for (int d = R - 1; d >= 1; --d) h[d] = h[d - 1];
+                    h[0] = y;
+                }
+            }
+        } else {
+            // ---------------- producers: thread q owns off-line slot line q
+            const int pw = warp - 2;   // producer warp index
+            const int q = tid - 64;
+            const int ql = FWD ? q : NQ + 1 + q;           // slot-line index (oy, oz)
+            const int oy = ql % W - R, oz = ql / W - R;
+#ifdef LP_S3_NOACTIVE
+            const bool active = false;
+#else
+            const bool active = q < NQ && ly + oy >= 0 && ly + oy < K && lz + oz >= 0 && lz + oz < K;
+#endif
+            const double *src = a.out + (active ? (int64_t)(L + oy + (int64_t)K * oz) * K : 0);
+            // processing coordinate p' -> x: forward x = p', backward x = K-1-p'
+            auto srcp = [&](int pp) { return src + (FWD ? pp : K - 1 - pp); };
+            auto fetch = [&](int pp) {
+                return (active && pp >= 0 && pp < K) ? ld_l2(srcp(pp), pol_keep) : 0.0;
+            };
+            double win[W];   // win[(p' mod W)]
+            double yq[P3];   // loads issued P3 rows ahead
+            double yr[PR3];  // re-polls issued PR3 rows ahead (used when yq came back empty)
+#pragma unroll
+            for (int j = 0; j < W; ++j) win[j] = 0.0;
+            // positions 0 .. R-1 (window of step 0 except its newest value)
+#pragma unroll
+            for (int pp = 0; pp < R; ++pp) win[pp % W] = fetch(pp);   // all loads in flight first
+#pragma unroll
+            for (int j = 0; j < P3; ++j) yq[j] = fetch(R + j);
+#pragma unroll
+            for (int j = 0; j < PR3; ++j) yr[j] = yq[j];
+#pragma unroll
+            for (int pp = 0; pp < R; ++pp)
+                if (active && pp < K) win[pp % W] = wait_value(srcp(pp), win[pp % W]);
+            const int coff = ql * W;   // slot of (ox = -R) in this slot line, relative to `base`
+            for (int u0 = 0; u0 < K; u0 += W) {
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    const int u = u0 + k;
+                    if (u < K) {
+                        const long long gs = gstep + u;
+                        const int slot = (int)(gs % NR);
+                        const int x = FWD ? u : K - 1 - u;
+                        const int64_t i = row0 + x;
+                        // newest window value p' = u + R (consumed P3 steps after its load)
+                        {
+                            const int pp = u + R;
+                            // A source line just ahead of this one leaves the deep load
+                            // empty; the re-poll issued PR3 rows ahead (always, so
+                            // nothing waits on the deep load's result to decide) usually
+                            // has it, and only if both are empty does the thread spin.
+                            double v = yq[k % P3];
+                            if (is_sent(v)) v = yr[k % PR3];
+#ifndef LP_S3_NOSPIN
+                            if (active && pp < K) v = wait_value(srcp(pp), v);
+#endif
+                            win[(k + R) % W] = v;
+                            yq[k % P3] = fetch(pp + P3);
+                            yr[k % PR3] = fetch(pp + PR3);
+                        }
+#ifdef LP_SWEEP_TRACE
+                    if (t == 1 && u < 64 && lane == 27 && pw == NPW - 1) a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 3] = gtime_dep(win[(k + R) % W]);
+#endif
+                        wait_row(slot, gs);
+                        const int sh = (int)(((i * S + base) & 1));
+#ifdef LP_SWEEP_TRACE
+                    if (t == 1 && u < 64 && lane == 27 && pw == NPW - 1) a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 4] = gtime_s3();
+#endif
+                        const unsigned rowa = ring_s + (unsigned)(slot * ROWD + sh + coff - base) * 8;
+                        double s0 = 0.0, s1 = 0.0;
+                        if (q < NQ) {
+#pragma unroll
+                            for (int j = 0; j < W; ++j) {
+                                // slot ox = j - R pairs with x + ox, i.e. p' = u + (FWD ? ox : -ox)
+                                const int d = FWD ? j - R : R - j;
+                                const double lv = lds(rowa + (unsigned)j * 8);
+                                if (j & 1) s1 = __fma_rn(lv, win[((k + d) % W + W) % W], s1);
+                                else s0 = __fma_rn(lv, win[((k + d) % W + W) % W], s0);
+                            }
+                        }
+                        double s = s0 + s1;
+#ifdef LP_SWEEP_TRACE
+                        if (t == 1 && u < 64 && lane == 27 && pw == NPW - 1)
+                            a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 6] = gtime_dep(s);
+#endif
+#pragma unroll
+                        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+#ifdef LP_SWEEP_TRACE
+                    if (t == 1 && u < 64 && lane == 27 && pw == NPW - 1) a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 5] = gtime_dep(s);
+#endif
+                        if (lane == 0) {
+                            atomicAdd(&slotdone[slot], 1);
+                            sts_v(red_s + (unsigned)((int)(gs % RRED) * NPW + pw) * 8, s);
+#ifdef LP_SWEEP_TRACE
+                            if ((t == 0 || t == nlines / 2) && u < 32)
+                                a.trace[(size_t)nlines * 8 + 256 + (t ? 32 * 8 : 0) + u * 8 + pw] = gtime_s3();
+#endif
+                        }
+                    }
+                }
+            }
+        }
+        gstep += K;
+        __syncthreads();
+    }
+}
+
+template <bool FWD, int R>
+int launch3(const Sweep3Args &a, cudaStream_t st) {
+    using G = S3<R>;
+    static int nblocks = 0;
+    static size_t smem_set = 0;
+    const size_t smem = ((size_t)G::NR * G::ROWD + a.g.K) * sizeof(double);
+    LP_ARG(smem <= 227 * 1024, "3-D sweep needs %zu bytes of shared memory (K = %d)", smem, a.g.K);
+    auto kern = box_sweep3d_kernel<FWD, R>;
+    if (smem > smem_set) {   // the rhs staging grows with the line length K
+        LP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 1, dev = 0, nsm = 148;
+        LP_CUDA(cudaGetDevice(&dev));
+        LP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::NT, smem));
+        if (occ < 1) return LP_ERR_ARG;
+        nblocks = occ * nsm;
+        smem_set = smem;
+    }
+    int blocks = nblocks < a.g.nlines ? nblocks : a.g.nlines;
+    kern<<<blocks, G::NT, smem, st>>>(a);
+    count_launch();
+    LP_CHECK_LAUNCH();
+    return LP_OK;
+}
+
+template <bool FWD>
+int dispatch3(const Sweep3Args &a, int r, cudaStream_t st) {
+    switch (r) {
+        case 2: return launch3<FWD, 2>(a, st);
+        case 3: return launch3<FWD, 3>(a, st);
+        case 4: return launch3<FWD, 4>(a, st);
+        case 5: return launch3<FWD, 5>(a, st);
+        case 6: return launch3<FWD, 6>(a, st);
+        case 7: return launch3<FWD, 7>(a, st);
+        case 8: return launch3<FWD, 8>(a, st);
+        case 9: return launch3<FWD, 9>(a, st);
+        case 10: return launch3<FWD, 10>(a, st);
+        default: return LP_ERR_ARG;
+    }
+}
+
+}  // namespace
+
+bool box_sweep3d_applies(const Geom &g) {
+    return g.d == 3 && g.r >= 2 && g.r <= 10 && g.K >= 1;
+}
+
+// The caller has pre-filled `out` with the sentinel and reset the ticket.
+int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket, cudaStream_t st) {
+    Geom g = geom_of(m->box);
+    if (!box_sweep3d_applies(g)) return LP_ERR_ARG;
+    Sweep3Args a;
+    a.g = g;
+    a.lu = m->box.lu;
+    a.rhs = rhs;
+    a.out = out;
+    a.ticket = ticket;
+    a.trace = nullptr;
+#ifdef LP_SWEEP_TRACE
+    {
+        static unsigned long long *tr = nullptr;
+        static size_t trn = 0;
+        if (trn < (size_t)g.nlines * 8 + 2048) {
+            if (tr) dfree(tr);
+            trn = (size_t)g.nlines * 8 + 2048;
+            dalloc(&tr, trn, "sweep trace");
+        }
+        cudaMemsetAsync(tr, 0, trn * 8, st);
+        a.trace = tr;
+        g_trace = tr;
+        g_trace_n = trn;
+    }
+#endif
+    return fwd ? dispatch3<true>(a, g.r, st) : dispatch3<false>(a, g.r, st);
+}
+
+}  // namespace lp

@@ -57,6 +57,25 @@ __device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
 }
 
+// L2 cache policies (createpolicy): streamed-once data evict_first, reused data evict_last
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ void bulk_g2s_hint(unsigned dst, const void *src, unsigned bytes, unsigned mbar,
+                                              unsigned long long pol) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                 " [%0], [%1], %2, [%3], %4;"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(unsigned a) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
@@ -64,6 +83,19 @@ __device__ __forceinline__ void mbar_arrive(unsigned a) {
 __device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
     asm volatile("{\n .reg .pred p;\n LP_W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
                  " @!p bra LP_W%=;\n}" ::"r"(a), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_test(unsigned a, unsigned parity) {
+    unsigned ok;
+    asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    return ok != 0;
+}
+
+// wait with back-off: for a warp whose spinning would take issue slots from
+// the warps it is waiting for
+__device__ __forceinline__ void mbar_wait_sleep(unsigned a, unsigned parity, unsigned ns) {
+    while (!mbar_test(a, parity)) __nanosleep(ns);
 }
 
 // ---- thread-block clusters (distributed shared memory)
