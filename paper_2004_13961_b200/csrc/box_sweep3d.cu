@@ -27,6 +27,8 @@
 // reverse, the upper half of each row, division by the diagonal).
 #include <math.h>
 
+#include <vector>
+
 #include "box_geom.cuh"
 #include "ilu.cuh"
 #include "smem_tma.cuh"
@@ -85,6 +87,7 @@ struct Sweep3Args {
     const double *rhs;
     double *out;
     int *ticket;
+    const int *order;            // ticket -> forward line index (wavefront order)
     unsigned long long *trace;   // LP_SWEEP_TRACE: [nlines][8] (ticket time, rows 0 / K/4 / K/2 / K-1 done)
 };
 
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_
         const int t = sh_line;
         __syncthreads();
         if (t >= nlines) return;
-        const int L = FWD ? t : nlines - 1 - t;
+        const int L = FWD ? a.order[t] : nlines - 1 - a.order[t];
         const int ly = L % K, lz = L / K;
         const int64_t row0 = (int64_t)L * K;
 #ifdef LP_SWEEP_TRACE
@@ -439,16 +442,45 @@ bool box_sweep3d_applies(const Geom &g) {
     return g.d == 3 && g.r >= 2 && g.r <= 10 && g.K >= 1;
 }
 
+// Wavefront order of the x-lines.  With unit cost per row, row (x, y, z) can
+// run at level x + (r+1) y + (r+1)^2 z, so line (y, z) starts at
+// (r+1)(y + (r+1) z): lines with equal key y + (r+1) z are independent, and
+// every line a line depends on -- (y', z) with y' < y, or (y', z') with z' < z
+// and y' <= y + r -- has a smaller key.  Handing lines out in key order keeps
+// the ~(r+2)K/(r+1)^2 planes of the wavefront in flight together (natural order
+// would hold the running CTAs to one or two planes) while every line still only
+// waits on lines with smaller tickets.  The backward sweep mirrors the order.
+static int ensure_line_order(BoxLayout &b, cudaStream_t st) {
+    if (b.line_order) return LP_OK;
+    const int K = b.K, r = b.r;
+    std::vector<int> ord;
+    ord.reserve((size_t)K * K);
+    for (int key = 0; key <= (K - 1) + (r + 1) * (K - 1); ++key)
+        for (int z = 0; z < K; ++z) {
+            const int y = key - (r + 1) * z;
+            if (y < 0) break;
+            if (y < K) ord.push_back(y + K * z);
+        }
+    int rc = dalloc(&b.line_order, ord.size(), "sweep line order");
+    if (rc) return rc;
+    LP_CUDA(cudaMemcpyAsync(b.line_order, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    LP_CUDA(cudaStreamSynchronize(st));
+    return LP_OK;
+}
+
 // The caller has pre-filled `out` with the sentinel and reset the ticket.
 int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket, cudaStream_t st) {
     Geom g = geom_of(m->box);
     if (!box_sweep3d_applies(g)) return LP_ERR_ARG;
+    int rc = ensure_line_order(m->box, st);
+    if (rc) return rc;
     Sweep3Args a;
     a.g = g;
     a.lu = m->box.lu;
     a.rhs = rhs;
     a.out = out;
     a.ticket = ticket;
+    a.order = m->box.line_order;
     a.trace = nullptr;
 #ifdef LP_SWEEP_TRACE
     {

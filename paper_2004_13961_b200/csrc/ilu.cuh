@@ -24,6 +24,8 @@ struct BoxLayout {
     // compact in-line bands of the factors for the sweeps' serial recurrence:
     // band_lo[row][q] = L(row, row-1-q), band_up[row][q] = U(row, row+1+q), q < r
     double *band_lo = nullptr, *band_up = nullptr, *diag = nullptr;
+    // 3-D sweeps: x-lines in wavefront order (see box_sweep3d.cu)
+    int *line_order = nullptr;
 };
 
 }  // namespace lp
