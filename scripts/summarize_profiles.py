@@ -12,8 +12,11 @@ src = "gpurun_out/"
 
 
 def table(path):
-    """Rows of an ncu --csv log (skips ==PROF==/==WARNING== lines)."""
-    lines = [ln for ln in open(path) if ln.startswith('"')]
+    """Rows of an ncu --csv log (skips ==PROF==/==WARNING== lines); [] if absent."""
+    try:
+        lines = [ln for ln in open(path) if ln.startswith('"')]
+    except FileNotFoundError:
+        return []
     return list(csv.reader(io.StringIO("".join(lines))))
 
 
@@ -73,3 +76,30 @@ for name in ("sweep", "ilu", "mv"):
         print(open(f"profiles/{tag}_{name}_full.csv").read())
     except FileNotFoundError:
         pass
+
+
+def summarize_rep(rep, out, note):
+    """Selected raw metrics of an `ncu -o` report into profiles/<out> (per launch)."""
+    import subprocess
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    if len(rows) < 3:
+        return
+    hdr = rows[0]
+    cols = ["Kernel Name"] + [k for k in keep if k in hdr]
+    idx = [hdr.index(c) for c in cols]
+    with open(f"profiles/{out}", "w") as f:
+        f.write(f"# {note}\n")
+        w = csv.writer(f)
+        w.writerow(cols)
+        for r in rows[1:]:
+            w.writerow([r[i] for i in idx])
+    print(open(f"profiles/{out}").read())
+
+
+if len(sys.argv) > 2:
+    # extra captures: <rep> <out.csv> <note>, repeated
+    extra = sys.argv[2:]
+    for k in range(0, len(extra) - 2, 3):
+        summarize_rep(extra[k], extra[k + 1], extra[k + 2])
