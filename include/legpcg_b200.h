@@ -83,6 +83,27 @@ int lp_operator_destroy(lp_operator *op);
  * u, out: device, K^d, x fastest.  out may not alias u. */
 int lp_apply(lp_operator *op, int which, const double *u, double *out, void *stream);
 
+/* ------------------------------------------------ slab-sharded 3-D matvec --
+ * apply_system (operator.py:204-210) split into the compute stages of a
+ * z-slab sharded schedule; the host runs the three
+ * all-to-alls between them (paper_2004_13961_b200/sharded.py).  All arrays
+ * are device, row-major in the listed axis order (last axis fastest).
+ *   forward:  u [nz][K][K]                      -> f0, f1, f2 [P][P][nz]
+ *   middle:   f0..f2 [ny][P][K] (y' slab y0..)  -> w0, w1, w2 [K][P][ny]
+ *   backward: w0..w2 [nkx][P][P]                -> out [K][K][nkx]
+ * Each line is computed exactly as by lp_apply, so the sharded product is
+ * bit-identical.  lp_copy2d copies a rows x cols block between leading
+ * dimensions lds and ldd (placement of received all-to-all chunks). */
+int lp_slab_forward(lp_operator *op, int which, int nz, const double *u, double *f0,
+                    double *f1, double *f2, void *stream);
+int lp_slab_middle(lp_operator *op, int which, int y0, int ny, const double *f0,
+                   const double *f1, const double *f2, double *w0, double *w1, double *w2,
+                   void *stream);
+int lp_slab_backward(lp_operator *op, int which, int nkx, const double *w0, const double *w1,
+                     const double *w2, double *out, void *stream);
+int lp_copy2d(int64_t rows, int cols, const double *src, int64_t lds, double *dst, int64_t ldd,
+              void *stream);
+
 /* ----------------------------------------------------- preconditioner --
  * General CSR matrix (SparseMatrix, sparse.py:38-86): upload and hold.
  * indptr[n+1], indices[nnz] (sorted per row), values[nnz]; host or device. */

@@ -64,6 +64,10 @@ _SIGS = {
     "lp_pcg_solve": (_i32, [_vp, _vp, _vp, _vp, _i32, _dbl, _i64, _vp,
                             ctypes.POINTER(LpReport), _vp]),
     "lp_dot": (_i32, [_i64, _vp, _vp, _vp, _vp]),
+    "lp_copy2d": (_i32, [_i64, _i32, _vp, _i64, _vp, _i64, _vp]),
+    "lp_slab_forward": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "lp_slab_middle": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "lp_slab_backward": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1,0 +1,198 @@
+"""Slab-sharded 3-D matvec over G ranks.
+
+Vectors (K^3, x fastest) are split into z-slabs, rank g holding planes
+[z0_g, z0_g + nz_g).  ``apply_system`` (operator.py:204-210) then runs as three
+compute stages between three all-to-alls (csrc/slab.cu has the layouts):
+
+  S1 S2 on the z-slab            -> 3 fields [y'][x'][z_g]      E1: y'-slabs
+  S3 (+ grids) B1 on a y'-slab   -> 3 fields [kx][z'][y'_g]     E2: kx-slabs
+  B2 B3 on a kx-slab             -> [kz][ky][kx_g]              E3: z-slabs
+
+Each rank's chunk for rank h is contiguous (the distributed axis is the
+slowest), so the exchanges are plain ``all_to_all_single`` calls over NCCL
+(NVLink/NVSwitch); ``lp_copy2d`` drops each received chunk into place.  Every
+line is computed by the same kernel as on one GPU, so the sharded matvec is
+bit-identical to ``apply_system``.
+
+``SlabMatvec`` holds the per-rank schedule; ``apply_local`` runs all G ranks
+in one process on one device with the exchanges done as device copies (the
+single-GPU emulation used by the GPU tests), ``apply_rank`` is one rank of a
+torch.distributed job.  PCG dot products across ranks use
+``distributed.ordered_dd_allreduce``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import _lib
+
+
+def slab_bounds(n, G):
+    """Balanced contiguous split of range(n) into G parts: list of (start, count)."""
+    base, extra = divmod(n, G)
+    out, s = [], 0
+    for g in range(G):
+        c = base + (1 if g < extra else 0)
+        out.append((s, c))
+        s += c
+    return out
+
+
+@dataclass
+class Schedule:
+    K: int
+    P: int
+    G: int
+
+    def __post_init__(self):
+        if self.G < 1 or self.G > self.K:
+            raise ValueError(f"cannot split {self.K} planes over {self.G} ranks")
+        self.z = slab_bounds(self.K, self.G)    # vectors and E3
+        self.y = slab_bounds(self.P, self.G)    # middle stage (y' nodes)
+        self.kx = slab_bounds(self.K, self.G)   # backward stage (kx modes)
+
+    # element counts of the chunks rank g sends to rank h in each exchange
+    def e1(self, g, h):
+        return self.y[h][1] * self.P * self.z[g][1]
+
+    def e2(self, g, h):
+        return self.kx[h][1] * self.P * self.y[g][1]
+
+    def e3(self, g, h):
+        return self.z[h][1] * self.K * self.kx[g][1]
+
+
+class SlabMatvec:
+    """(A+B) u for z-slab sharded u, on the device of the calling process."""
+
+    device = "cuda"
+
+    def __init__(self, spec, plan, G, which=3):
+        if spec.dim != 3:
+            raise ValueError("slab sharding is for the 3-D operator")
+        import torch
+        self.torch = torch
+        self.which = which
+        self.s = Schedule(spec.n_modes, plan.order, G)
+        self._setup(spec, plan)
+
+    def _setup(self, spec, plan):
+        self.lib = _lib.load()
+        self.op = spec.device_operator(plan)
+
+    # ---------------------------------------------------------------- stages
+    def _empty(self, n):
+        return self.torch.empty(max(n, 1), dtype=self.torch.float64, device=self.device)
+
+    def stage1(self, g, u_slab):
+        s = self.s
+        nz = s.z[g][1]
+        f = [self._empty(s.P * s.P * nz) for _ in range(3)]
+        _lib.check(self.lib.lp_slab_forward(self.op, self.which, nz, u_slab.data_ptr(),
+                                            f[0].data_ptr(), f[1].data_ptr(), f[2].data_ptr(),
+                                            _lib.stream_ptr()), "slab forward")
+        return f
+
+    def stage2(self, h, f_in):
+        s = self.s
+        y0, ny = s.y[h]
+        w = [self._empty(s.K * s.P * ny) for _ in range(3)]
+        _lib.check(self.lib.lp_slab_middle(self.op, self.which, y0, ny, f_in[0].data_ptr(),
+                                           f_in[1].data_ptr(), f_in[2].data_ptr(),
+                                           w[0].data_ptr(), w[1].data_ptr(), w[2].data_ptr(),
+                                           _lib.stream_ptr()), "slab middle")
+        return w
+
+    def stage3(self, h, w_in):
+        s = self.s
+        nkx = s.kx[h][1]
+        out = self._empty(s.K * s.K * nkx)
+        _lib.check(self.lib.lp_slab_backward(self.op, self.which, nkx, w_in[0].data_ptr(),
+                                             w_in[1].data_ptr(), w_in[2].data_ptr(),
+                                             out.data_ptr(), _lib.stream_ptr()), "slab backward")
+        return out
+
+    # ------------------------------------------------------------- placement
+    def _copy2d(self, rows, cols, src, dst, col, ld):
+        _lib.check(self.lib.lp_copy2d(rows, cols, src.data_ptr(), cols, dst.data_ptr() + 8 * col,
+                                      ld, _lib.stream_ptr()), "copy2d")
+
+    def _place(self, chunks, rows_of, cols_of, ld, n_out):
+        """Received chunks (one per source rank, [rows][cols_g]) -> [rows][ld] at col offsets."""
+        out = self._empty(n_out)
+        col = 0
+        for g, c in enumerate(chunks):
+            cols = cols_of(g)
+            if cols and rows_of:
+                self._copy2d(rows_of, cols, c, out, col, ld)
+            col += cols
+        return out
+
+    def place_e1(self, h, chunks):
+        s = self.s
+        ny = s.y[h][1]
+        return self._place(chunks, ny * s.P, lambda g: s.z[g][1], s.K, ny * s.P * s.K)
+
+    def place_e2(self, h, chunks):
+        s = self.s
+        nkx = s.kx[h][1]
+        return self._place(chunks, nkx * s.P, lambda g: s.y[g][1], s.P, nkx * s.P * s.P)
+
+    def place_e3(self, h, chunks):
+        s = self.s
+        nz = s.z[h][1]
+        return self._place(chunks, nz * s.K, lambda g: s.kx[g][1], s.K, nz * s.K * s.K)
+
+    @staticmethod
+    def split(t, sizes):
+        out, o = [], 0
+        for n in sizes:
+            out.append(t[o:o + n])
+            o += n
+        return out
+
+    # ----------------------------------------------------------- schedules
+    def apply_local(self, u_slabs):
+        """All G ranks in this process (single-device emulation of the exchanges)."""
+        s, G = self.s, self.s.G
+        f = [self.stage1(g, u_slabs[g]) for g in range(G)]
+        sent = [[self.split(f[g][k], [s.e1(g, h) for h in range(G)]) for k in range(3)]
+                for g in range(G)]
+        mid = [[self.place_e1(h, [sent[g][k][h] for g in range(G)]) for k in range(3)]
+               for h in range(G)]
+        w = [self.stage2(h, mid[h]) for h in range(G)]
+        sent = [[self.split(w[g][k], [s.e2(g, h) for h in range(G)]) for k in range(3)]
+                for g in range(G)]
+        back = [[self.place_e2(h, [sent[g][k][h] for g in range(G)]) for k in range(3)]
+                for h in range(G)]
+        o = [self.stage3(h, back[h]) for h in range(G)]
+        sent = [self.split(o[g], [s.e3(g, h) for h in range(G)]) for g in range(G)]
+        return [self.place_e3(h, [sent[g][h] for g in range(G)]) for h in range(G)]
+
+    def apply_rank(self, rank, u_slab, group=None):
+        """One rank of a torch.distributed job: three NCCL all-to-alls."""
+        import torch.distributed as dist
+        s, G = self.s, self.s.G
+
+        def exchange(t, send_sizes, recv_sizes):
+            recv = self._empty(sum(recv_sizes))
+            dist.all_to_all_single(recv[:sum(recv_sizes)], t[:sum(send_sizes)],
+                                   output_split_sizes=recv_sizes,
+                                   input_split_sizes=send_sizes, group=group)
+            return self.split(recv, recv_sizes)
+
+        f = self.stage1(rank, u_slab)
+        mid = [self.place_e1(rank, exchange(f[k], [s.e1(rank, h) for h in range(G)],
+                                            [s.e1(g, rank) for g in range(G)])) for k in range(3)]
+        w = self.stage2(rank, mid)
+        back = [self.place_e2(rank, exchange(w[k], [s.e2(rank, h) for h in range(G)],
+                                             [s.e2(g, rank) for g in range(G)])) for k in range(3)]
+        o = self.stage3(rank, back)
+        return self.place_e3(rank, exchange(o, [s.e3(rank, h) for h in range(G)],
+                                            [s.e3(g, rank) for g in range(G)]))
+
+
+def split_vector(u_flat, K, G):
+    """z-slabs (views) of an x-fastest K^3 vector."""
+    return [u_flat[z0 * K * K:(z0 + nz) * K * K] for z0, nz in slab_bounds(K, G)]

@@ -1,0 +1,203 @@
+"""Slab-sharded 3-D matvec (paper_2004_13961_b200/sharded.py, csrc/slab.cu).
+
+CPU (gloo, world_size 2): the exchange schedule -- chunk sizes, all-to-all
+splits, placement of received chunks -- run with numpy stand-ins for the three
+compute stages (the same sum-factorised passes, test-only), checked against the
+CPU oracle's apply_system.  GPU: the CUDA stages, with the exchanges emulated
+on one device, are bit-identical to the single-GPU apply_system."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import legpcg_port as orc
+from paper_2004_13961_b200 import ProblemSpec, workloads as wl
+from paper_2004_13961_b200.sharded import Schedule, SlabMatvec, slab_bounds
+
+
+def spec_of(w, N):
+    return ProblemSpec(dim=w.dim, N=N, beta=w.beta, alpha=w.alpha)
+
+
+class NumpySlab(SlabMatvec):
+    """The stages of csrc/slab.cu restated with numpy einsum on CPU tensors."""
+
+    device = "cpu"
+
+    def _setup(self, spec, plan):
+        s = self.s
+        K, P = s.K, s.P
+        op = orc.Plan(P)
+        V = op.table
+        self.F = V[:, :K] - V[:, 2:K + 2]                                   # phi_k(x_i)
+        self.D = V[:, 1:K + 1] * (-(2.0 * np.arange(K) + 3.0))              # phi_k'(x_i)
+        w3 = np.einsum("i,j,l->ijl", op.weights, op.weights, op.weights)
+        b = orc.grid(spec, op, "beta") * w3                                 # [x][y][z]
+        self.bw = np.ascontiguousarray(b.transpose(2, 1, 0))               # [z][y][x]
+        self.aw = None
+        if spec.alpha is not None and not spec.alpha.is_zero:
+            a = np.broadcast_to(orc.grid(spec, op, "alpha"), (P, P, P)) * w3
+            self.aw = np.ascontiguousarray(a.transpose(2, 1, 0))
+
+    def _t(self, a):
+        return torch.from_numpy(np.ascontiguousarray(a).reshape(-1).copy())
+
+    def stage1(self, g, u_slab):
+        s, F, D = self.s, self.F, self.D
+        u = u_slab.numpy().reshape(s.z[g][1], s.K, s.K)                     # [z][y][x]
+        g0 = np.einsum("ax,zyx->azy", F, u)
+        g1 = np.einsum("ax,zyx->azy", D, u)
+        return [self._t(np.einsum("by,azy->baz", F, g1)), self._t(np.einsum("by,azy->baz", D, g0)),
+                self._t(np.einsum("by,azy->baz", F, g0))]
+
+    def stage2(self, h, f_in):
+        s, F, D = self.s, self.F, self.D
+        y0, ny = s.y[h]
+        f = [t.numpy().reshape(ny, s.P, s.K) for t in f_in]                 # [y'][x'][z]
+        bw = self.bw[:, y0:y0 + ny, :]
+        q0 = np.einsum("cz,yxz->cyx", F, f[0]) * bw
+        q1 = np.einsum("cz,yxz->cyx", F, f[1]) * bw
+        q2 = np.einsum("cz,yxz->cyx", D, f[2]) * bw
+        w0 = np.einsum("xk,cyx->kcy", D, q0)
+        if self.aw is not None:
+            w0 = w0 + np.einsum("xk,cyx->kcy", F, np.einsum("cz,yxz->cyx", F, f[2])
+                                * self.aw[:, y0:y0 + ny, :])
+        return [self._t(w0), self._t(np.einsum("xk,cyx->kcy", F, q1)),
+                self._t(np.einsum("xk,cyx->kcy", F, q2))]
+
+    def stage3(self, h, w_in):
+        s, F, D = self.s, self.F, self.D
+        nkx = s.kx[h][1]
+        w = [t.numpy().reshape(nkx, s.P, s.P) for t in w_in]               # [kx][z'][y']
+        v0 = np.einsum("yk,xcy->kxc", F, w[0]) + np.einsum("yk,xcy->kxc", D, w[1])
+        v1 = np.einsum("yk,xcy->kxc", F, w[2])
+        return self._t(np.einsum("ck,yxc->kyx", F, v0) + np.einsum("ck,yxc->kyx", D, v1))
+
+    def _copy2d(self, rows, cols, src, dst, col, ld):
+        dst[:rows * ld].view(rows, ld)[:, col:col + cols] = src[:rows * cols].view(rows, cols)
+
+
+def _problem(name="cfg5", N=14, seed=3):
+    w = wl.CONFIGS[name]()
+    spec = spec_of(w, N)
+    K = N - 1
+    u = np.random.default_rng(seed).standard_normal((K, K, K))             # oracle: [x][y][z]
+    ref = orc.apply_system(spec, orc.Plan(N + 1), u)
+    flat = np.ascontiguousarray(u.transpose(2, 1, 0)).reshape(-1)           # x fastest
+    ref_flat = np.ascontiguousarray(ref.transpose(2, 1, 0)).reshape(-1)
+    return w, spec, flat, ref_flat
+
+
+def _slabs(flat, K, G):
+    return [torch.from_numpy(flat[z0 * K * K:(z0 + nz) * K * K].copy()) for z0, nz in slab_bounds(K, G)]
+
+
+def relerr(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def test_schedule_chunk_sizes():
+    for K, G in [(13, 1), (13, 2), (13, 3), (127, 8), (511, 8), (9, 9)]:
+        s = Schedule(K, K + 2, G)
+        for g in range(G):
+            assert sum(s.e1(g, h) for h in range(G)) == s.P * s.P * s.z[g][1]
+            assert sum(s.e2(g, h) for h in range(G)) == s.K * s.P * s.y[g][1]
+            assert sum(s.e3(g, h) for h in range(G)) == s.K * s.K * s.kx[g][1]
+        for h in range(G):
+            assert sum(s.e1(g, h) for g in range(G)) == s.y[h][1] * s.P * s.K
+    with pytest.raises(ValueError):
+        Schedule(4, 6, 5)
+
+
+@pytest.mark.parametrize("G", [1, 2, 3])
+@pytest.mark.parametrize("name", ["cfg4", "cfg5"])
+def test_sharded_schedule_numpy_local(name, G):
+    w, spec, flat, ref = _problem(name, N=12)
+    K = spec.n_modes
+    sm = _numpy_slab(spec, G)
+    out = torch.cat(sm.apply_local(_slabs(flat, K, G))).numpy()
+    assert relerr(out, ref) < 1e-12
+
+
+def _numpy_slab(spec, G):
+    sm = NumpySlab.__new__(NumpySlab)
+    sm.torch = torch
+    sm.which = 3
+    sm.s = Schedule(spec.n_modes, spec.N + 1, G)
+    sm._setup(spec, None)
+    return sm
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, ws, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(ws),
+                      RANK=str(rank), LOCAL_RANK=str(rank))
+    from paper_2004_13961_b200 import distributed as Dm
+    dist = Dm.init("gloo")
+    try:
+        w, spec, flat, ref = _problem("cfg5", N=14)
+        K = spec.n_modes
+        sm = _numpy_slab(spec, ws)
+        mine = sm.apply_rank(rank, _slabs(flat, K, ws)[rank])
+        out[rank] = mine[:K * K * slab_bounds(K, ws)[rank][1]].numpy().tobytes()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(240)
+def test_gloo_two_ranks_sharded_matvec():
+    ws = 2
+    port = _free_port()
+    import torch.multiprocessing as mp
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_worker, args=(ws, port, out), nprocs=ws, join=True)
+        res = dict(out)
+    got = np.concatenate([np.frombuffer(res[r], dtype=np.float64) for r in range(ws)])
+    w, spec, flat, ref = _problem("cfg5", N=14)
+    assert relerr(got, ref) < 1e-12
+    # the exchanges over gloo give exactly the single-process schedule's bits
+    local = torch.cat(_numpy_slab(spec, ws).apply_local(_slabs(flat, spec.n_modes, ws))).numpy()
+    assert np.array_equal(got, local)
+
+
+# ----------------------------------------------------------------------- GPU
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,N", [("cfg4", 24), ("cfg5", 20)])
+@pytest.mark.parametrize("G", [1, 2, 3, 4])
+def test_cuda_stages_bit_identical(name, N, G):
+    from paper_2004_13961_b200 import TransformPlan
+    from paper_2004_13961_b200.operator import apply_flat
+    w = wl.CONFIGS[name]()
+    spec = spec_of(w, N)
+    plan = TransformPlan(N + 1)
+    K = N - 1
+    u = torch.randn(K ** 3, dtype=torch.float64, device="cuda",
+                    generator=torch.Generator(device="cuda").manual_seed(7))
+    full = apply_flat(spec, plan, 3, u)
+    sm = SlabMatvec(spec, plan, G)
+    slabs = [u[z0 * K * K:(z0 + nz) * K * K].contiguous() for z0, nz in slab_bounds(K, G)]
+    out = torch.cat([o[:K * K * nz] for o, (_, nz) in zip(sm.apply_local(slabs), slab_bounds(K, G))])
+    assert torch.equal(out, full)
+
+
+@pytest.mark.gpu
+def test_cuda_stages_match_oracle():
+    from paper_2004_13961_b200 import TransformPlan
+    w, spec, flat, ref = _problem("cfg5", N=14)
+    plan = TransformPlan(15)
+    K = 13
+    u = torch.from_numpy(flat).cuda()
+    sm = SlabMatvec(spec, plan, 3)
+    slabs = [u[z0 * K * K:(z0 + nz) * K * K].contiguous() for z0, nz in slab_bounds(K, 3)]
+    out = torch.cat([o[:K * K * nz] for o, (_, nz) in zip(sm.apply_local(slabs), slab_bounds(K, 3))])
+    assert relerr(out.cpu().numpy(), ref) < 1e-12
