@@ -104,6 +104,17 @@ int lp_slab_backward(lp_operator *op, int which, int nkx, const double *w0, cons
 int lp_copy2d(int64_t rows, int cols, const double *src, int64_t lds, double *dst, int64_t ldd,
               void *stream);
 
+/* forward_sub (dir 0) / backward_sub (dir 1) of 3-D box factors with the vector
+ * distributed over nranks y-slab ranks (rank v owns the x-lines with y in
+ * [ys[v], ys[v+1])), emulated on one device in one launch: `out` holds nranks
+ * replicas of n values (replica v at out + v*n); each line is computed from its
+ * owner's replica and stored to the owner and to every rank whose stencil halo
+ * [ys[u] - r, ys[u+1] + r) contains it -- the stores a multi-GPU run makes into
+ * its neighbours' memory.  rhs: one vector, or nranks replicas when
+ * rhs_replicated != 0.  Results equal lp_forward_sub / lp_backward_sub. */
+int lp_sweep_ranks(lp_ilu *f, int nranks, const int *ys, int dir, const double *rhs,
+                   int rhs_replicated, double *out, void *stream);
+
 /* ----------------------------------------------------- preconditioner --
  * General CSR matrix (SparseMatrix, sparse.py:38-86): upload and hold.
  * indptr[n+1], indices[nnz] (sorted per row), values[nnz]; host or device. */
@@ -164,6 +175,12 @@ int lp_pcg_solve(lp_operator *op, lp_ilu *precond, const double *F, double *x,
 /* --------------------------------------------------------- vector ops --
  * Building blocks exposed for tests and for host-driven loops. */
 /* out[0..1] (device) = double-double sum_i a_i b_i, deterministic order. */
+/* PCG vector updates with host scalars (sharded driver, sharded.py):
+ * p = z (first != 0) or z + beta p;  x += alpha p, r -= alpha w with the
+ * double-double r'r of the slab in out2[0..1] (device). */
+int lp_update_p(int64_t n, const double *z, double *p, double beta, int first, void *stream);
+int lp_update_xr(int64_t n, double *x, double *r, const double *p, const double *w, double alpha,
+                 double *out2, void *stream);
 int lp_dot(int64_t n, const double *a, const double *b, double *out2, void *stream);
 
 #ifdef __cplusplus

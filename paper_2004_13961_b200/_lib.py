@@ -65,6 +65,9 @@ _SIGS = {
                             ctypes.POINTER(LpReport), _vp]),
     "lp_dot": (_i32, [_i64, _vp, _vp, _vp, _vp]),
     "lp_copy2d": (_i32, [_i64, _i32, _vp, _i64, _vp, _i64, _vp]),
+    "lp_sweep_ranks": (_i32, [_vp, _i32, _vp, _i32, _vp, _i32, _vp, _vp]),
+    "lp_update_p": (_i32, [_i64, _vp, _vp, _dbl, _i32, _vp]),
+    "lp_update_xr": (_i32, [_i64, _vp, _vp, _vp, _vp, _dbl, _vp, _vp]),
     "lp_slab_forward": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "lp_slab_middle": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "lp_slab_backward": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),

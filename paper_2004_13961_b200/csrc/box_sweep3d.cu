@@ -54,6 +54,7 @@ __device__ __forceinline__ unsigned long long gtime_s3() {
 
 constexpr unsigned long long SENT3 = 0xFFF4C0FFEE5EED00ull;   // = SWEEP_SENTINEL (box_sweep.cu)
 constexpr int RRED = 16;   // rows of warp sums in flight
+constexpr int MAX_RANKS = 8;
 
 template <int R>
 struct S3 {
@@ -88,6 +89,14 @@ struct Sweep3Args {
     double *out;
     int *ticket;
     const int *order;            // ticket -> forward line index (wavefront order)
+    // y-slab ranks: rank v owns the lines with y in [ys[v], ys[v+1]).
+    // Every rank keeps a replica of the vector (replica v at out + v * rep_stride,
+    // rhs likewise at rhs + v * rhs_stride); a line is read from and written to
+    // its owner's replica and also written to every rank whose stencil halo
+    // [ys[u] - r, ys[u+1] + r) contains it.  nranks = 1 is the plain sweep.
+    int nranks;
+    int ys[MAX_RANKS + 1];
+    int64_t rep_stride, rhs_stride;
     unsigned long long *trace;   // LP_SWEEP_TRACE: [nlines][8] (ticket time, rows 0 / K/4 / K/2 / K-1 done)
 };
 
@@ -181,6 +190,10 @@ __global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_
         const int L = FWD ? a.order[t] : nlines - 1 - a.order[t];
         const int ly = L % K, lz = L / K;
         const int64_t row0 = (int64_t)L * K;
+        int owner = 0;
+        while (owner + 1 < a.nranks && ly >= a.ys[owner + 1]) ++owner;
+        double *const out = a.out + owner * a.rep_stride;    // this line's replica
+        const double *const rhs = a.rhs + owner * a.rhs_stride;
 #ifdef LP_SWEEP_TRACE
         if (tid == 0) a.trace[(size_t)t * 8] = gtime_s3();
 #endif
@@ -229,7 +242,7 @@ __global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_
         } else if (warp == 1) {
             // ---------------- serial warp: in-line recurrence (lane 0)
             // the line's right-hand side, one coalesced pass into shared memory
-            for (int x = lane; x < K; x += 32) rhs_s[x] = __ldcg(a.rhs + row0 + x);
+            for (int x = lane; x < K; x += 32) rhs_s[x] = __ldcg(rhs + row0 + x);
             __syncwarp();
             if (lane == 0) {
                 double h[R];   // h[d-1] = output of the row d steps back in processing order
@@ -275,7 +288,10 @@ __global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_
 #endif
                     if (FWD ? x >= 1 : x + 1 < K) acc = __fma_rn(-c1, h[0], acc);
                     const double y = canon3(FWD ? acc : __ddiv_rn(acc, diag));
-                    st_keep(a.out + i, y, pol_keep);
+                    st_keep(out + i, y, pol_keep);
+                    for (int v = 0; v < a.nranks; ++v)   // halo copies (multi-rank only)
+                        if (v != owner && ly >= a.ys[v] - R && ly < a.ys[v + 1] + R)
+                            st_keep(a.out + v * a.rep_stride + i, y, pol_keep);
 #ifdef LP_SWEEP_TRACE
                     if (t == 1 && u < 64) a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 2] = gtime_s3();
 #endif
@@ -301,7 +317,7 @@ __global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_
 #else
             const bool active = q < NQ && ly + oy >= 0 && ly + oy < K && lz + oz >= 0 && lz + oz < K;
 #endif
-            const double *src = a.out + (active ? (int64_t)(L + oy + (int64_t)K * oz) * K : 0);
+            const double *src = out + (active ? (int64_t)(L + oy + (int64_t)K * oz) * K : 0);
             // processing coordinate p' -> x: forward x = p', backward x = K-1-p'
             auto srcp = [&](int pp) { return src + (FWD ? pp : K - 1 - pp); };
             auto fetch = [&](int pp) {
@@ -481,6 +497,17 @@ int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket
     a.out = out;
     a.ticket = ticket;
     a.order = m->box.line_order;
+    a.nranks = 1;
+    a.ys[0] = 0;
+    a.ys[1] = g.K;
+    a.rep_stride = 0;
+    a.rhs_stride = 0;
+    if (m->sweep_nranks > 1) {
+        a.nranks = m->sweep_nranks;
+        for (int v = 0; v <= a.nranks; ++v) a.ys[v] = m->sweep_ys[v];
+        a.rep_stride = g.n;
+        a.rhs_stride = m->sweep_rhs_replicated ? g.n : 0;
+    }
     a.trace = nullptr;
 #ifdef LP_SWEEP_TRACE
     {
@@ -500,4 +527,44 @@ int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket
     return fwd ? dispatch3<true>(a, g.r, st) : dispatch3<false>(a, g.r, st);
 }
 
+namespace {
+__global__ void fill_sent3(int64_t n, double *a) {
+    const double v = __longlong_as_double((long long)SENT3);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = v;
+}
+}  // namespace
+
 }  // namespace lp
+
+using namespace lp;
+
+// Sweeps with the vector distributed over y-slab ranks,
+// emulated on one device in one launch: rank v owns the x-lines with y in
+// [ys[v], ys[v+1]) and keeps a replica of the vector (replica v of `out` at
+// out + v n); a line is computed from its owner's replica and published to the
+// owner and to every rank whose stencil halo reaches it, exactly the stores a
+// multi-GPU run makes into its neighbours' memory over NVLink.  rhs is one
+// vector (forward) or nranks replicas (backward, rhs_replicated = 1).
+extern "C" int lp_sweep_ranks(lp_ilu *f, int nranks, const int *ys, int dir, const double *rhs,
+                              int rhs_replicated, double *out, void *stream) {
+    LP_ARG(f->kind == MAT_BOX && f->factored, "lp_sweep_ranks needs a factored box matrix");
+    Geom g = geom_of(f->box);
+    LP_ARG(box_sweep3d_applies(g), "lp_sweep_ranks is for 3-D box factors (reach 2..10)");
+    LP_ARG(nranks >= 1 && nranks <= MAX_RANKS, "nranks must be in 1..%d", MAX_RANKS);
+    LP_ARG(ys[0] == 0 && ys[nranks] == g.K, "y slabs must cover [0, K)");
+    for (int v = 0; v < nranks; ++v) LP_ARG(ys[v] < ys[v + 1], "empty y slab");
+    cudaStream_t st = as_stream(stream);
+    fill_sent3<<<148 * 8, 256, 0, st>>>((int64_t)nranks * g.n, out);
+    count_launch();
+    int *tk = f->ticket + (dir == 0 ? 0 : 1);
+    LP_CUDA(cudaMemsetAsync(tk, 0, sizeof(int), st));
+    f->sweep_nranks = nranks;
+    for (int v = 0; v <= nranks; ++v) f->sweep_ys[v] = ys[v];
+    f->sweep_rhs_replicated = rhs_replicated != 0;
+    const int rc = box_sweep3d(f, dir == 0, rhs, out, tk, st);
+    f->sweep_nranks = 1;
+    f->sweep_rhs_replicated = false;
+    return rc;
+}
+

@@ -49,6 +49,10 @@ struct lp_ilu {
     int64_t *bad = nullptr;     // zero-pivot key (device)
     double *ytmp = nullptr;     // forward-sweep result for precond_apply
     int64_t missing_diag = -1;  // first row without a stored diagonal (box assembly)
+    // 3-D sweeps over y-slab ranks emulated on one device (lp_sweep_ranks)
+    int sweep_nranks = 1;
+    int sweep_ys[9] = {0};
+    bool sweep_rhs_replicated = false;
 };
 
 namespace lp {

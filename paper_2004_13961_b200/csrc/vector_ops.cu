@@ -122,3 +122,61 @@ extern "C" int lp_dot(int64_t n, const double *a, const double *b, double *out2,
     cudaFreeAsync(partial, st);
     return rc;
 }
+
+// ---- host-scalar variants for the sharded PCG driver (sharded.py): the
+// scalars come from rank-ordered double-double reductions on the host.
+namespace lp {
+namespace {
+
+__global__ void axpby_p_kernel(int64_t n, const double *__restrict__ z, double *__restrict__ p,
+                               double beta, int first) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = first ? z[i] : __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+}
+
+__global__ void __launch_bounds__(RED_THREADS)
+update_xr_host_kernel(int64_t n, double *__restrict__ x, double *__restrict__ r,
+                      const double *__restrict__ p, const double *__restrict__ w, double alpha,
+                      double *__restrict__ partial) {
+    dd acc{0.0, 0.0};
+    for (int64_t i = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x; i < n;
+         i += (int64_t)RED_BLOCKS * RED_THREADS) {
+        x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+        const double ri = __dsub_rn(r[i], __dmul_rn(alpha, w[i]));
+        r[i] = ri;
+        acc = dd_add_prod(acc, ri, ri);
+    }
+    acc = block_reduce_dd(acc);
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = acc.hi;
+        partial[2 * blockIdx.x + 1] = acc.lo;
+    }
+}
+
+}  // namespace
+}  // namespace lp
+
+// p = z (first) or z + beta p  (pcg.py:150-155 with beta = rho / rho_old)
+extern "C" int lp_update_p(int64_t n, const double *z, double *p, double beta, int first,
+                           void *stream) {
+    cudaStream_t st = lp::as_stream(stream);
+    lp::axpby_p_kernel<<<lp::grid_for(n), 256, 0, st>>>(n, z, p, beta, first);
+    lp::count_launch();
+    LP_CHECK_LAUNCH();
+    return LP_OK;
+}
+
+// x += alpha p, r -= alpha w (pcg.py:161-162); out2 = double-double r'r of this slab
+extern "C" int lp_update_xr(int64_t n, double *x, double *r, const double *p, const double *w,
+                            double alpha, double *out2, void *stream) {
+    cudaStream_t st = lp::as_stream(stream);
+    double *partial;
+    LP_CUDA(cudaMallocAsync((void **)&partial, 2 * lp::RED_BLOCKS * sizeof(double), st));
+    lp::update_xr_host_kernel<<<lp::RED_BLOCKS, lp::RED_THREADS, 0, st>>>(n, x, r, p, w, alpha,
+                                                                         partial);
+    lp::count_launch();
+    int rc = lp::finalize_dd(partial, out2, st);
+    cudaFreeAsync(partial, st);
+    return rc;
+}

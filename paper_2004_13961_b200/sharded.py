@@ -196,3 +196,125 @@ class SlabMatvec:
 def split_vector(u_flat, K, G):
     """z-slabs (views) of an x-fastest K^3 vector."""
     return [u_flat[z0 * K * K:(z0 + nz) * K * K] for z0, nz in slab_bounds(K, G)]
+
+
+# ------------------------------------------------------------------ PCG
+
+def _dd_add(x, y):
+    from .distributed import dd_add
+    return dd_add(x, y)
+
+
+class SlabSweeps:
+    """The ILU(0) sweeps with the vector over G y-slab ranks (lp_sweep_ranks):
+    rank v owns the x-lines with y in its slab of [0, K) and a replica of the
+    vector; every line is published to its owner and to the ranks whose
+    stencil halo (+-r lines) reaches it.  Emulated on one device."""
+
+    def __init__(self, factors, K, G):
+        import torch
+        self.torch = torch
+        self.lib = _lib.load()
+        self.f = factors
+        self.K, self.G = K, G
+        self.ys = [z0 for z0, _ in slab_bounds(K, G)] + [K]
+        import ctypes
+        self._ys = (ctypes.c_int * (G + 1))(*self.ys)
+        n = K ** 3
+        self.yrep = torch.empty(G * n, dtype=torch.float64, device="cuda")
+        self.zrep = torch.empty(G * n, dtype=torch.float64, device="cuda")
+
+    def apply(self, r_full):
+        """z = M^-1 r; r_full is the assembled residual (what the y-slab owners
+        hold after the z-slab -> y-slab exchange); returns the assembled z."""
+        lib, K, G = self.lib, self.K, self.G
+        _lib.check(lib.lp_sweep_ranks(self.f._handle, G, self._ys, 0, r_full.data_ptr(), 0,
+                                      self.yrep.data_ptr(), _lib.stream_ptr()), "forward sweep")
+        _lib.check(lib.lp_sweep_ranks(self.f._handle, G, self._ys, 1, self.yrep.data_ptr(), 1,
+                                      self.zrep.data_ptr(), _lib.stream_ptr()), "backward sweep")
+        return self.gather(self.zrep)
+
+    def gather(self, reps):
+        """Each rank's own lines from its replica -> one x-fastest vector."""
+        K, G = self.K, self.G
+        n = K ** 3
+        out = self.torch.empty(n, dtype=self.torch.float64, device="cuda")
+        for v in range(G):
+            y0, ny = self.ys[v], self.ys[v + 1] - self.ys[v]
+            _lib.check(self.lib.lp_copy2d(K, ny * K, reps.data_ptr() + 8 * (v * n + y0 * K), K * K,
+                                          out.data_ptr() + 8 * y0 * K, K * K, _lib.stream_ptr()),
+                       "gather")
+        return out
+
+
+def pcg_solve_sharded_local(spec, config, plan, f_flat, G, factors=None):
+    """PCG (pcg.py:111-179) with every stage distributed over G ranks, emulated
+    on one device: the matvec z-slab sharded (SlabMatvec, three all-to-alls),
+    the sweeps over y-slab ranks with halo publication (SlabSweeps), vector
+    updates per z-slab (lp_update_p / lp_update_xr) and the three dots per
+    iteration as per-slab double-double partials combined in rank order (what
+    ordered_dd_allreduce does across processes).  Returns (x_full, report)."""
+    import math
+
+    import torch
+    from .pcg import setup_preconditioner
+    lib = _lib.load()
+    K = spec.n_modes
+    n = K ** 3
+    sm = SlabMatvec(spec, plan, G)
+    if factors is None:
+        factors = setup_preconditioner(spec, config, plan)
+    sw = SlabSweeps(factors, K, G) if factors is not None else None
+    zb = slab_bounds(K, G)
+    cut = [(z0 * K * K, nz * K * K) for z0, nz in zb]
+    st = _lib.stream_ptr
+    two = torch.empty(2, dtype=torch.float64, device="cuda")
+
+    def dot(a, b):
+        """sum over ranks (rank order) of per-slab double-double a.b"""
+        acc = (0.0, 0.0)
+        for o, c in cut:
+            _lib.check(lib.lp_dot(c, a.data_ptr() + 8 * o, b.data_ptr() + 8 * o, two.data_ptr(), st()))
+            h = two.cpu().numpy()
+            acc = _dd_add(acc, (float(h[0]), float(h[1])))
+        return acc[0]
+
+    def matvec(u):
+        outs = sm.apply_local([u[o:o + c] for o, c in cut])
+        return torch.cat([w[:c] for w, (o, c) in zip(outs, cut)])
+
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    r = f_flat.clone()
+    p = torch.empty_like(r)
+    fnorm = math.sqrt(dot(f_flat, f_flat))
+    rr = dot(r, r)
+    hist = [math.sqrt(rr)]
+    tol = config.epsilon * fnorm
+    it, rho_old = 0, None
+    while math.sqrt(rr) > tol and it < config.k_max:
+        z = sw.apply(r) if sw is not None else r
+        it += 1
+        rho = dot(r, z)
+        beta = 0.0 if it == 1 else rho / rho_old
+        for o, c in cut:
+            _lib.check(lib.lp_update_p(c, z.data_ptr() + 8 * o, p.data_ptr() + 8 * o, beta,
+                                       int(it == 1), st()))
+        w = matvec(p)
+        curv = dot(p, w)
+        if curv <= 0.0:
+            from .pcg import IndefiniteOperatorError
+            raise IndefiniteOperatorError(it, curv)
+        alpha = rho / curv
+        acc = (0.0, 0.0)
+        for o, c in cut:
+            _lib.check(lib.lp_update_xr(c, x.data_ptr() + 8 * o, r.data_ptr() + 8 * o,
+                                        p.data_ptr() + 8 * o, w.data_ptr() + 8 * o, alpha,
+                                        two.data_ptr(), st()))
+            h = two.cpu().numpy()
+            acc = _dd_add(acc, (float(h[0]), float(h[1])))
+        rr = acc[0]
+        rho_old = rho
+        hist.append(math.sqrt(rr))
+    return x, {"iterations": it, "converged": math.sqrt(rr) <= tol,
+               "final_relative_residual": math.sqrt(rr) / fnorm if fnorm else 0.0,
+               "residual_history": hist, "ranks": G}

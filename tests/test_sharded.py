@@ -201,3 +201,56 @@ def test_cuda_stages_match_oracle():
     slabs = [u[z0 * K * K:(z0 + nz) * K * K].contiguous() for z0, nz in slab_bounds(K, 3)]
     out = torch.cat([o[:K * K * nz] for o, (_, nz) in zip(sm.apply_local(slabs), slab_bounds(K, 3))])
     assert relerr(out.cpu().numpy(), ref) < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,N,T,G", [("cfg4", 24, 8, 2), ("cfg4", 24, 8, 3), ("cfg5", 20, 3, 4),
+                                        ("cfg4", 40, 8, 4)])
+def test_rank_sweeps_bit_identical(name, N, T, G):
+    """Sweeps over G y-slab ranks with halo publication == the one-rank sweeps."""
+    from paper_2004_13961_b200 import TransformPlan, _lib
+    from paper_2004_13961_b200.precond import assemble_M
+    from paper_2004_13961_b200.sharded import SlabSweeps
+    from paper_2004_13961_b200.sparse import ilu0
+    w = wl.CONFIGS[name]()
+    spec = spec_of(w, N)
+    f = ilu0(assemble_M(spec, T, T, TransformPlan(N + 1)))
+    K = N - 1
+    n = K ** 3
+    r = torch.randn(n, dtype=torch.float64, device="cuda",
+                    generator=torch.Generator(device="cuda").manual_seed(5))
+    lib = _lib.load()
+    y1 = torch.empty_like(r)
+    z1 = torch.empty_like(r)
+    _lib.check(lib.lp_forward_sub(f._handle, r.data_ptr(), y1.data_ptr(), _lib.stream_ptr()))
+    _lib.check(lib.lp_backward_sub(f._handle, y1.data_ptr(), z1.data_ptr(), _lib.stream_ptr()))
+    sw = SlabSweeps(f, K, G)
+    z = sw.apply(r)
+    assert torch.equal(sw.gather(sw.yrep), y1)
+    assert torch.equal(z, z1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,N,T,G", [("cfg4", 24, 8, 2), ("cfg5", 20, 8, 3), ("cfg4", 32, 8, 4)])
+def test_sharded_pcg_matches_single_gpu(name, N, T, G):
+    """The fully distributed PCG (emulated on one GPU) against the one-GPU solve
+    and the CPU oracle: same iteration count (+-1), solution within 1e-10."""
+    from paper_2004_13961_b200 import SolverConfig, TransformPlan, device
+    from paper_2004_13961_b200.pcg import pcg_solve_device, setup_preconditioner
+    from paper_2004_13961_b200.sharded import pcg_solve_sharded_local
+    w = wl.CONFIGS[name]()
+    spec = spec_of(w, N)
+    plan = TransformPlan(N + 1)
+    cfg = SolverConfig(epsilon=w.rtol, preconditioner=(T, T))
+    F = wl.mass_contract_series(wl.seeded_fhat(3, N + 1))
+    fd = device.to_device(F.flatten(order="F"))
+    fac = setup_preconditioner(spec, cfg, plan)
+    x1, r1 = pcg_solve_device(spec, cfg, plan, fd, factors=fac)
+    xg, rg = pcg_solve_sharded_local(spec, cfg, plan, fd, G, factors=fac)
+    assert abs(rg["iterations"] - r1["iterations"]) <= 1
+    assert rg["converged"]
+    assert relerr(xg.cpu().numpy(), x1.cpu().numpy()) < 1e-10
+    if N <= 24:
+        xo, ro = orc.pcg_solve(spec, F, epsilon=w.rtol, preconditioner=(T, T))
+        assert abs(rg["iterations"] - ro["iterations"]) <= 1
+        assert relerr(xg.cpu().numpy(), np.asarray(xo).flatten(order="F")) < 1e-10
