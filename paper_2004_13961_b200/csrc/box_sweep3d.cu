@@ -466,7 +466,7 @@ bool box_sweep3d_applies(const Geom &g) {
 // the ~(r+2)K/(r+1)^2 planes of the wavefront in flight together (natural order
 // would hold the running CTAs to one or two planes) while every line still only
 // waits on lines with smaller tickets.  The backward sweep mirrors the order.
-static int ensure_line_order(BoxLayout &b, cudaStream_t st) {
+int ensure_line_order(BoxLayout &b, cudaStream_t st) {
     if (b.line_order) return LP_OK;
     const int K = b.K, r = b.r;
     std::vector<int> ord;

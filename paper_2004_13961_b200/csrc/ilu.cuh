@@ -69,5 +69,6 @@ int box_ilu0_2d_tasks(lp_ilu *m, double tol, unsigned long long *key, const unsi
 int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_t st);
 struct Geom;
 bool box_sweep3d_applies(const Geom &g);
+int ensure_line_order(BoxLayout &b, cudaStream_t st);
 int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket, cudaStream_t st);
 }  // namespace lp
