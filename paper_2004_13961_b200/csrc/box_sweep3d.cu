@@ -80,6 +80,11 @@ struct S3 {
     static constexpr int P = W % 7 == 0 ? 7 : W;
     static constexpr int PR = 1;   // measured (cfg-4 recipe, N=64): 1 row 17.9 ms, 3 rows 22.0 ms per pair
 #endif
+#ifdef LP_S3_MINB
+    static constexpr int MINB = R <= 4 ? LP_S3_MINB : 1;
+#else
+    static constexpr int MINB = 1;
+#endif
 };
 
 struct Sweep3Args {
@@ -136,7 +141,7 @@ __device__ __forceinline__ double wait_value(const double *p, double v) {
 }
 
 template <bool FWD, int R>
-__global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_constant__ Sweep3Args a) {
+__global__ void __launch_bounds__(S3<R>::NT, S3<R>::MINB) box_sweep3d_kernel(const __grid_constant__ Sweep3Args a) {
     using G = S3<R>;
     constexpr int W = G::W, S = G::S, C = G::C, NQ = G::NQ, NPW = G::NPW, ROWD = G::ROWD, NR = G::NR;
     constexpr int P3 = G::P, PR3 = G::PR;
