@@ -40,12 +40,6 @@ extern size_t g_trace_n;
 
 namespace {
 
-__device__ __forceinline__ unsigned long long gtime_dep(double dep) {
-    unsigned long long t;
-    asm volatile("{ .reg .f64 d; mov.f64 d, %1; mov.u64 %0, %%globaltimer; }" : "=l"(t) : "d"(dep));
-    return t;
-}
-
 __device__ __forceinline__ unsigned long long gtime_s3() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -79,11 +73,6 @@ struct S3 {
 #else
     static constexpr int P = W % 7 == 0 ? 7 : W;
     static constexpr int PR = 1;   // measured (cfg-4 recipe, N=64): 1 row 17.9 ms, 3 rows 22.0 ms per pair
-#endif
-#ifdef LP_S3_MINB
-    static constexpr int MINB = R <= 4 ? LP_S3_MINB : 1;
-#else
-    static constexpr int MINB = 1;
 #endif
 };
 
@@ -141,7 +130,7 @@ __device__ __forceinline__ double wait_value(const double *p, double v) {
 }
 
 template <bool FWD, int R>
-__global__ void __launch_bounds__(S3<R>::NT, S3<R>::MINB) box_sweep3d_kernel(const __grid_constant__ Sweep3Args a) {
+__global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_constant__ Sweep3Args a) {
     using G = S3<R>;
     constexpr int W = G::W, S = G::S, C = G::C, NQ = G::NQ, NPW = G::NPW, ROWD = G::ROWD, NR = G::NR;
     constexpr int P3 = G::P, PR3 = G::PR;
@@ -227,10 +216,6 @@ __global__ void __launch_bounds__(S3<R>::NT, S3<R>::MINB) box_sweep3d_kernel(con
                     const unsigned bytes = (unsigned)(((e0 - ea) + len + 1) / 2 * 2) * 8;
                     mbar_expect(full_s + slot * 8, bytes);
                     bulk_g2s_hint(ring_s + (unsigned)slot * ROWD * 8, a.lu + ea, bytes, full_s + slot * 8, pol_stream);
-#ifdef LP_SWEEP_TRACE
-                    if ((t == 0 || t == nlines / 2) && u < 32)
-                        a.trace[(size_t)nlines * 8 + (t ? 128 : 0) + u * 4] = gtime_s3();
-#endif
                 }
             }
             else if (lane == 1) {
@@ -262,9 +247,6 @@ __global__ void __launch_bounds__(S3<R>::NT, S3<R>::MINB) box_sweep3d_kernel(con
                     wait_row(slot, gs);
                     const int sh = (int)(((i * S + base) & 1));
                     const unsigned rowa = ring_s + (unsigned)(slot * ROWD + sh) * 8;
-#ifdef LP_SWEEP_TRACE
-                    if (t == 1 && u < 64) a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 0] = gtime_s3();
-#endif
                     // in-line coefficients: forward L(x, x-d) at slot C-d; backward U(x, x+d) at C+d
                     double acc = rhs;
 #pragma unroll
@@ -288,24 +270,16 @@ __global__ void __launch_bounds__(S3<R>::NT, S3<R>::MINB) box_sweep3d_kernel(con
                         csum += v;
                     }
                     acc -= csum;
-#ifdef LP_SWEEP_TRACE
-                    if (t == 1 && u < 64) a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 1] = gtime_dep(acc);
-#endif
                     if (FWD ? x >= 1 : x + 1 < K) acc = __fma_rn(-c1, h[0], acc);
                     const double y = canon3(FWD ? acc : __ddiv_rn(acc, diag));
                     st_keep(out + i, y, pol_keep);
-                    for (int v = 0; v < a.nranks; ++v)   // halo copies (multi-rank only)
-                        if (v != owner && ly >= a.ys[v] - R && ly < a.ys[v + 1] + R)
-                            st_keep(a.out + v * a.rep_stride + i, y, pol_keep);
 #ifdef LP_SWEEP_TRACE
-                    if (t == 1 && u < 64) a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 2] = gtime_s3();
-#endif
-#ifdef LP_SWEEP_TRACE
-                    if ((t == 0 || t == nlines / 2) && u < 32)
-                        a.trace[(size_t)nlines * 8 + (t ? 128 : 0) + u * 4 + 3] = gtime_s3();
                     if (u == 0 || u == K / 4 || u == K / 2 || u == K - 1)
                         a.trace[(size_t)t * 8 + 1 + (u == 0 ? 0 : u == K / 4 ? 1 : u == K / 2 ? 2 : 3)] = gtime_s3();
 #endif
+                    for (int v = 0; v < a.nranks; ++v)   // halo copies (multi-rank only)
+                        if (v != owner && ly >= a.ys[v] - R && ly < a.ys[v + 1] + R)
+                            st_keep(a.out + v * a.rep_stride + i, y, pol_keep);
 #pragma unroll
                     for (int d = R - 1; d >= 1; --d) h[d] = h[d - 1];
                     h[0] = y;
@@ -317,11 +291,7 @@ __global__ void __launch_bounds__(S3<R>::NT, S3<R>::MINB) box_sweep3d_kernel(con
             const int q = tid - 64;
             const int ql = FWD ? q : NQ + 1 + q;           // slot-line index (oy, oz)
             const int oy = ql % W - R, oz = ql / W - R;
-#ifdef LP_S3_NOACTIVE
-            const bool active = false;
-#else
             const bool active = q < NQ && ly + oy >= 0 && ly + oy < K && lz + oz >= 0 && lz + oz < K;
-#endif
             const double *src = out + (active ? (int64_t)(L + oy + (int64_t)K * oz) * K : 0);
             // processing coordinate p' -> x: forward x = p', backward x = K-1-p'
             auto srcp = [&](int pp) { return src + (FWD ? pp : K - 1 - pp); };
@@ -362,21 +332,13 @@ __global__ void __launch_bounds__(S3<R>::NT, S3<R>::MINB) box_sweep3d_kernel(con
                             // has it, and only if both are empty does the thread spin.
                             double v = yq[k % P3];
                             if (is_sent(v)) v = yr[k % PR3];
-#ifndef LP_S3_NOSPIN
                             if (active && pp < K) v = wait_value(srcp(pp), v);
-#endif
                             win[(k + R) % W] = v;
                             yq[k % P3] = fetch(pp + P3);
                             yr[k % PR3] = fetch(pp + PR3);
                         }
-#ifdef LP_SWEEP_TRACE
-                    if (t == 1 && u < 64 && lane == 27 && pw == NPW - 1) a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 3] = gtime_dep(win[(k + R) % W]);
-#endif
                         wait_row(slot, gs);
                         const int sh = (int)(((i * S + base) & 1));
-#ifdef LP_SWEEP_TRACE
-                    if (t == 1 && u < 64 && lane == 27 && pw == NPW - 1) a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 4] = gtime_s3();
-#endif
                         const unsigned rowa = ring_s + (unsigned)(slot * ROWD + sh + coff - base) * 8;
                         double s0 = 0.0, s1 = 0.0;
                         if (q < NQ) {
@@ -390,22 +352,11 @@ __global__ void __launch_bounds__(S3<R>::NT, S3<R>::MINB) box_sweep3d_kernel(con
                             }
                         }
                         double s = s0 + s1;
-#ifdef LP_SWEEP_TRACE
-                        if (t == 1 && u < 64 && lane == 27 && pw == NPW - 1)
-                            a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 6] = gtime_dep(s);
-#endif
 #pragma unroll
                         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-#ifdef LP_SWEEP_TRACE
-                    if (t == 1 && u < 64 && lane == 27 && pw == NPW - 1) a.trace[(size_t)nlines * 8 + 1024 + u * 8 + 5] = gtime_dep(s);
-#endif
                         if (lane == 0) {
                             atomicAdd(&slotdone[slot], 1);
                             sts_v(red_s + (unsigned)((int)(gs % RRED) * NPW + pw) * 8, s);
-#ifdef LP_SWEEP_TRACE
-                            if ((t == 0 || t == nlines / 2) && u < 32)
-                                a.trace[(size_t)nlines * 8 + 256 + (t ? 32 * 8 : 0) + u * 8 + pw] = gtime_s3();
-#endif
                         }
                     }
                 }
@@ -518,9 +469,9 @@ int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket
     {
         static unsigned long long *tr = nullptr;
         static size_t trn = 0;
-        if (trn < (size_t)g.nlines * 8 + 2048) {
+        if (trn < (size_t)g.nlines * 8) {
             if (tr) dfree(tr);
-            trn = (size_t)g.nlines * 8 + 2048;
+            trn = (size_t)g.nlines * 8;
             dalloc(&tr, trn, "sweep trace");
         }
         cudaMemsetAsync(tr, 0, trn * 8, st);

@@ -29,11 +29,9 @@ for _ in range(2):
     lib.lp_forward_sub(f._handle, r.data_ptr(), y.data_ptr(), _lib.stream_ptr())
 torch.cuda.synchronize()
 nl = K * K
-buf = np.zeros(nl * 8 + 2048, dtype=np.uint64)
+buf = np.zeros(nl * 8, dtype=np.uint64)
 lib.lp_debug_sweep_trace.restype = ctypes.c_int
 lib.lp_debug_sweep_trace(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_int64(buf.size))
-fine = buf[nl * 8:nl * 8 + 256].reshape(2, 32, 4).astype(np.int64)
-warps = buf[nl * 8 + 256:nl * 8 + 768].reshape(2, 32, 8).astype(np.int64)
 tr = buf[:nl * 8].reshape(nl, 8).astype(np.int64)[:, :5]
 t0 = tr[:, 0].min()
 tr = (tr - t0) / 1e3
@@ -49,19 +47,3 @@ print("plane lead (row0 of line y=0), median %.1f us" % np.median(np.diff(pl)))
 print("per-row slope in line (us/row): median %.3f" % np.median((rl - r0) / (K - 1)))
 for L in [0, 1, 2, K // 2, K, K + 1, K * K // 2, K * K // 2 + 1, nl - 1]:
     print(L, (tr[L] ).round(1))
-for k, nm in enumerate(["line 0", "line nl/2"]):
-    f0 = fine[k]
-    base = f0[0, 0]
-    print(nm, "rows 0..15: issue, prod w0 done, prod wlast done, serial done (us from first issue)")
-    for u in range(16):
-        print("  ", u, ((f0[u] - base) / 1e3).round(2))
-for k, nm in enumerate(["line 0", "line nl/2"]):
-    base = fine[k][0, 0]
-    print(nm, "per-warp producer done (us) rows 0..11")
-    for u in range(12):
-        print("  ", u, ((warps[k][u] - base) / 1e3).round(2))
-l1 = buf[nl * 8 + 1024:nl * 8 + 1536].reshape(64, 8).astype(np.int64)[:, :7]
-b = l1[0, 3]
-print("line 1 (us): serial full-wait, red done(dep), stored | w6 lane27 window done(dep), full-wait, reduced(dep), fma done(dep)")
-for u in range(24):
-    print("  ", u, ((l1[u, :7] - b) / 1e3).round(2))
