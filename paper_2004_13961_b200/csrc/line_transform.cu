@@ -97,7 +97,12 @@ __device__ __forceinline__ void store_tile(const Prefetch &pf, double *stage, in
     }
 }
 
-__global__ void __launch_bounds__(THREADS, 1)
+// MINB = 2 caps registers at 128 (a few spilled) so two CTAs share an SM:
+// measured on B200, cfg 5 matvec 69.1 -> 52.7 ms (50 -> 66 % of DGEMM peak), cfg 3
+// 4.57 -> 3.61 ms; grids smaller than two waves keep the 1-CTA form (cfg 2: 0.118 vs
+// 0.139 ms).
+template <int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
 line_transform_kernel(const __grid_constant__ LtArgs a) {
     extern __shared__ __align__(16) double smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -367,14 +372,21 @@ void lt_set_out(LtArgs &a, int oi, double *out, const double *grid) {
 int line_transform(const LtArgs &a, cudaStream_t st) {
     static bool attr_set = false;
     if (!attr_set) {
-        LP_CUDA(cudaFuncSetAttribute(line_transform_kernel,
+        LP_CUDA(cudaFuncSetAttribute(line_transform_kernel<1>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)SMEM_BYTES));
+        LP_CUDA(cudaFuncSetAttribute(line_transform_kernel<2>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)SMEM_BYTES));
         attr_set = true;
     }
     if (a.B <= 0 || a.nouts <= 0) return LP_OK;
     dim3 grid((unsigned)ceil_div(a.B, BN), (unsigned)(a.Mdim / BM), (unsigned)a.nouts);
-    line_transform_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(a);
+    const int64_t ctas = (int64_t)grid.x * grid.y * grid.z;
+    if (ctas > 2 * 148)
+        line_transform_kernel<2><<<grid, THREADS, SMEM_BYTES, st>>>(a);
+    else
+        line_transform_kernel<1><<<grid, THREADS, SMEM_BYTES, st>>>(a);
     count_launch();
     LP_CHECK_LAUNCH();
     return LP_OK;
