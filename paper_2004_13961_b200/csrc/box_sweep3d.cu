@@ -83,6 +83,8 @@ struct Sweep3Args {
     double *out;
     int *ticket;
     const int *order;            // ticket -> forward line index (wavefront order)
+    const int *gpos;             // small reach: group g = lines order[gpos[g] .. gpos[g+1])
+    int ngroups;
     // y-slab ranks: rank v owns the lines with y in [ys[v], ys[v+1]).
     // Every rank keeps a replica of the vector (replica v at out + v * rep_stride,
     // rhs likewise at rhs + v * rhs_stride); a line is read from and written to
@@ -367,6 +369,285 @@ __global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_
     }
 }
 
+
+// ---------------------------------------------------------------- small reach
+// For r <= 4 a row is only (2r+1)^3 / 2 entries (62 at r = 2), so one line per CTA
+// leaves most lanes idle and the per-row overhead dominates.  This variant takes a
+// group of up to LPB lines with the SAME wavefront key (independent of each other)
+// and advances them in lockstep: one TMA copy per line per step, producer lane
+// (line j, source q) in segments of NQP lanes, serial lane j runs line j.
+template <int R>
+struct S3m {
+    static constexpr int W = 2 * R + 1, W2 = W * W, S = W2 * W, C = (S - 1) / 2;
+    static constexpr int NQ = R * W + R;
+    static constexpr int NQP = NQ <= 16 ? 16 : NQ <= 32 ? 32 : 64;     // lanes per line
+    static constexpr int LPB = NQP <= 16 ? 8 : 4;                      // lines per CTA
+    static constexpr int NPW = LPB * NQP / 32;
+    static constexpr int PPL = NQP > 32 ? NQP / 32 : 1;               // partial sums per line
+    static constexpr int NT = 32 * (NPW + 2);
+    static constexpr int ROWD = (C + 1 + 1 + 1) / 2 * 2;
+    static constexpr int NR = 6;
+    static constexpr int P = W;   // window look-ahead (divides W)
+};
+
+template <bool FWD, int R>
+__global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const __grid_constant__ Sweep3Args a) {
+    using G = S3m<R>;
+    constexpr int W = G::W, S = G::S, C = G::C, NQ = G::NQ, NQP = G::NQP, LPB = G::LPB;
+    constexpr int NPW = G::NPW, PPL = G::PPL, ROWD = G::ROWD, NR = G::NR, P3 = G::P;
+    extern __shared__ __align__(16) double ring[];          // [NR][LPB][ROWD], then rhs [LPB][K]
+    __shared__ __align__(8) unsigned long long mbar[NR];
+    __shared__ double red[RRED][LPB][PPL];
+    __shared__ int rowready[NR];
+    __shared__ int slotdone[NR];
+    __shared__ int sh_grp;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int K = a.g.K;
+    const int nlines = a.g.nlines;
+    const unsigned ring_s = smem_addr(ring);
+    double *rhs_s = ring + NR * LPB * ROWD;
+    const unsigned full_s = smem_addr(mbar);
+    if (tid == 0) {
+        for (int q = 0; q < NR; ++q) mbar_init(full_s + q * 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int q = tid; q < NR; q += blockDim.x) {
+        rowready[q] = -1;
+        slotdone[q] = 0;
+    }
+    for (int q = tid; q < RRED * LPB * PPL; q += blockDim.x)
+        (&red[0][0][0])[q] = __longlong_as_double((long long)SENT3);
+    __syncthreads();
+    const unsigned red_s = smem_addr(&red[0][0][0]);
+    auto wait_row = [&](int slot, long long gs) {
+        const unsigned fa = smem_addr(&rowready[slot]);
+        int f;
+        do {
+            asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(f) : "r"(fa) : "memory");
+        } while (f != (int)gs);
+    };
+    constexpr int base = FWD ? 0 : C;
+    constexpr int len = FWD ? C : C + 1;
+    long long gstep = 0;
+    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    for (;;) {
+        if (tid == 0) sh_grp = atomicAdd(a.ticket, 1);
+        __syncthreads();
+        const int t = sh_grp;
+        __syncthreads();
+        if (t >= a.ngroups) return;
+        const int gp = a.gpos[t], cnt = a.gpos[t + 1] - gp;
+        auto line_of = [&](int j) { return FWD ? a.order[gp + j] : nlines - 1 - a.order[gp + j]; };
+        auto owner_of = [&](int ly) {
+            int v = 0;
+            while (v + 1 < a.nranks && ly >= a.ys[v + 1]) ++v;
+            return v;
+        };
+
+        if (warp == 0) {
+            if (lane == 0) {
+                for (int u = 0; u < K; ++u) {
+                    const long long gs = gstep + u;
+                    const int slot = (int)(gs % NR);
+                    if (gs >= NR) {
+                        const int need = (int)(gs / NR) * (NPW + 1);
+                        const unsigned ca = smem_addr(&slotdone[slot]);
+                        int f;
+                        for (;;) {
+                            asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(f) : "r"(ca) : "memory");
+                            if (f >= need) break;
+                            __nanosleep(32);
+                        }
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    }
+                    const int x = FWD ? u : K - 1 - u;
+                    unsigned total = 0;
+                    for (int j = 0; j < cnt; ++j) {
+                        const int64_t e0 = ((int64_t)line_of(j) * K + x) * S + base;
+                        total += (unsigned)(((e0 & 1) + len + 1) / 2 * 2) * 8;
+                    }
+                    mbar_expect(full_s + slot * 8, total);
+                    for (int j = 0; j < cnt; ++j) {
+                        const int64_t e0 = ((int64_t)line_of(j) * K + x) * S + base;
+                        const int64_t ea = e0 & ~(int64_t)1;
+                        const unsigned bytes = (unsigned)(((e0 - ea) + len + 1) / 2 * 2) * 8;
+                        bulk_g2s_hint(ring_s + (unsigned)((slot * LPB + j) * ROWD) * 8, a.lu + ea, bytes,
+                                      full_s + slot * 8, pol_stream);
+                    }
+                }
+            } else if (lane == 1) {
+                for (int u = 0; u < K; ++u) {
+                    const long long gs = gstep + u;
+                    const int slot = (int)(gs % NR);
+                    mbar_wait(full_s + slot * 8, (unsigned)((gs / NR) & 1));
+                    asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(smem_addr(&rowready[slot])), "r"((int)gs)
+                                 : "memory");
+                }
+            }
+        } else if (warp == 1) {
+            // ---------------- serial warp: lane j runs line j
+            for (int e = lane; e < cnt * K; e += 32) {
+                const int j = e / K, x = e - j * K;
+                const int L = line_of(j);
+                const double *rh = a.rhs + owner_of(L % K) * a.rhs_stride;
+                rhs_s[j * K + x] = __ldcg(rh + (int64_t)L * K + x);
+            }
+            __syncwarp();
+            const bool mine = lane < cnt;
+            const int L = mine ? line_of(lane) : 0;
+            const int ly = L % K;
+            const int owner = owner_of(ly);
+            double *const out = a.out + owner * a.rep_stride;
+            const int64_t row0 = (int64_t)L * K;
+            double h[R];
+#pragma unroll
+            for (int d = 0; d < R; ++d) h[d] = 0.0;
+            for (int u = 0; u < K; ++u) {
+                const long long gs = gstep + u;
+                const int slot = (int)(gs % NR);
+                const int x = FWD ? u : K - 1 - u;
+                const int64_t i = row0 + x;
+                wait_row(slot, gs);
+                double acc = 0.0, c1 = 0.0, diag = 1.0;
+                if (mine) {
+                    acc = rhs_s[lane * K + x];
+                    const int sh = (int)((i * S + base) & 1);
+                    const unsigned rowa = ring_s + (unsigned)((slot * LPB + lane) * ROWD + sh) * 8;
+#pragma unroll
+                    for (int d = R; d >= 2; --d) {
+                        const bool ok = FWD ? x - d >= 0 : x + d < K;
+                        const double cf = lds(rowa + (unsigned)(FWD ? C - d : d) * 8);
+                        if (ok) acc = __fma_rn(-cf, h[d - 1], acc);
+                    }
+                    c1 = lds(rowa + (unsigned)(FWD ? C - 1 : 1) * 8);
+                    if (!FWD) diag = lds(rowa);
+                }
+                __syncwarp();
+                if (lane == 0) atomicAdd(&slotdone[slot], 1);
+                if (mine) {
+                    const int rr = (int)(gs % RRED);
+                    double csum = 0.0;
+#pragma unroll
+                    for (int w = 0; w < PPL; ++w) {
+                        const unsigned ra = red_s + (unsigned)((rr * LPB + lane) * PPL + w) * 8;
+                        double v = lds_v(ra);
+                        while (is_sent(v)) v = lds_v(ra);
+                        sts_v(ra, __longlong_as_double((long long)SENT3));
+                        csum += v;
+                    }
+                    acc -= csum;
+                    if (FWD ? x >= 1 : x + 1 < K) acc = __fma_rn(-c1, h[0], acc);
+                    const double y = canon3(FWD ? acc : __ddiv_rn(acc, diag));
+                    st_keep(out + i, y, pol_keep);
+                    for (int v = 0; v < a.nranks; ++v)
+                        if (v != owner && ly >= a.ys[v] - R && ly < a.ys[v + 1] + R)
+                            st_keep(a.out + v * a.rep_stride + i, y, pol_keep);
+#pragma unroll
+                    for (int d = R - 1; d >= 1; --d) h[d] = h[d - 1];
+                    h[0] = y;
+                }
+            }
+        } else {
+            // ---------------- producers: lane (j, q) = source q of line j
+            const int p = tid - 64;
+            const int pw = warp - 2;
+            const int j = p / NQP, q = p % NQP;
+            const int ql = FWD ? q : NQ + 1 + q;
+            const int oy = ql % W - R, oz = ql / W - R;
+            const int L = j < cnt ? line_of(j) : 0;
+            const int ly = L % K, lz = L / K;
+            const bool active = j < cnt && q < NQ && ly + oy >= 0 && ly + oy < K && lz + oz >= 0 && lz + oz < K;
+            const double *out = a.out + owner_of(ly) * a.rep_stride;
+            const double *src = out + (active ? (int64_t)(L + oy + (int64_t)K * oz) * K : 0);
+            auto srcp = [&](int pp) { return src + (FWD ? pp : K - 1 - pp); };
+            auto fetch = [&](int pp) {
+                return (active && pp >= 0 && pp < K) ? ld_l2(srcp(pp), pol_keep) : 0.0;
+            };
+            double win[W], yq[P3], yr = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) win[k] = 0.0;
+#pragma unroll
+            for (int pp = 0; pp < R; ++pp) win[pp % W] = fetch(pp);
+#pragma unroll
+            for (int k = 0; k < P3; ++k) yq[k] = fetch(R + k);
+            yr = yq[0];
+#pragma unroll
+            for (int pp = 0; pp < R; ++pp)
+                if (active && pp < K) win[pp % W] = wait_value(srcp(pp), win[pp % W]);
+            const int coff = ql * W;
+            const int64_t row0 = (int64_t)L * K;
+            for (int u0 = 0; u0 < K; u0 += W) {
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    const int u = u0 + k;
+                    if (u < K) {
+                        const long long gs = gstep + u;
+                        const int slot = (int)(gs % NR);
+                        const int x = FWD ? u : K - 1 - u;
+                        const int64_t i = row0 + x;
+                        {
+                            const int pp = u + R;
+                            double v = yq[k % P3];
+                            if (is_sent(v)) v = yr;
+                            if (active && pp < K) v = wait_value(srcp(pp), v);
+                            win[(k + R) % W] = v;
+                            yq[k % P3] = fetch(pp + P3);
+                            yr = fetch(pp + 1);
+                        }
+                        wait_row(slot, gs);
+                        double s0 = 0.0, s1 = 0.0;
+                        if (active) {
+                            const int sh = (int)((i * S + base) & 1);
+                            const unsigned rowa = ring_s + (unsigned)((slot * LPB + j) * ROWD + sh + coff - base) * 8;
+#pragma unroll
+                            for (int jj = 0; jj < W; ++jj) {
+                                const int d = FWD ? jj - R : R - jj;
+                                const double lv = lds(rowa + (unsigned)jj * 8);
+                                if (jj & 1) s1 = __fma_rn(lv, win[((k + d) % W + W) % W], s1);
+                                else s0 = __fma_rn(lv, win[((k + d) % W + W) % W], s0);
+                            }
+                        }
+                        double sum = s0 + s1;
+#pragma unroll
+                        for (int o = (NQP < 32 ? NQP : 32) / 2; o; o >>= 1)
+                            sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                        if (lane == 0) atomicAdd(&slotdone[slot], 1);
+                        if ((q & 31) == 0 && j < cnt)
+                            sts_v(red_s + (unsigned)(((int)(gs % RRED) * LPB + j) * PPL + (q >> 5)) * 8, sum);
+                    }
+                }
+            }
+        }
+        gstep += K;
+        __syncthreads();
+    }
+}
+
+template <bool FWD, int R>
+int launch3m(const Sweep3Args &a, cudaStream_t st) {
+    using G = S3m<R>;
+    static int nblocks = 0;
+    static size_t smem_set = 0;
+    const size_t smem = ((size_t)G::NR * G::LPB * G::ROWD + (size_t)G::LPB * a.g.K) * sizeof(double);
+    LP_ARG(smem <= 227 * 1024, "3-D sweep needs %zu bytes of shared memory (K = %d)", smem, a.g.K);
+    auto kern = box_sweep3d_multi_kernel<FWD, R>;
+    if (smem > smem_set) {
+        LP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 1, dev = 0, nsm = 148;
+        LP_CUDA(cudaGetDevice(&dev));
+        LP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::NT, smem));
+        if (occ < 1) return LP_ERR_ARG;
+        nblocks = occ * nsm;
+        smem_set = smem;
+    }
+    int blocks = nblocks < a.ngroups ? nblocks : a.ngroups;
+    kern<<<blocks, G::NT, smem, st>>>(a);
+    count_launch();
+    LP_CHECK_LAUNCH();
+    return LP_OK;
+}
+
 template <bool FWD, int R>
 int launch3(const Sweep3Args &a, cudaStream_t st) {
     using G = S3<R>;
@@ -395,9 +676,9 @@ int launch3(const Sweep3Args &a, cudaStream_t st) {
 template <bool FWD>
 int dispatch3(const Sweep3Args &a, int r, cudaStream_t st) {
     switch (r) {
-        case 2: return launch3<FWD, 2>(a, st);
-        case 3: return launch3<FWD, 3>(a, st);
-        case 4: return launch3<FWD, 4>(a, st);
+        case 2: return launch3m<FWD, 2>(a, st);
+        case 3: return launch3m<FWD, 3>(a, st);
+        case 4: return launch3m<FWD, 4>(a, st);
         case 5: return launch3<FWD, 5>(a, st);
         case 6: return launch3<FWD, 6>(a, st);
         case 7: return launch3<FWD, 7>(a, st);
@@ -440,12 +721,50 @@ int ensure_line_order(BoxLayout &b, cudaStream_t st) {
     return LP_OK;
 }
 
+// Groups of up to lpb consecutive lines of line_order with the same key (the
+// small-reach kernel advances a group in lockstep; equal keys are independent).
+static int ensure_line_groups(BoxLayout &b, int lpb, cudaStream_t st) {
+    if (b.line_groups) return LP_OK;
+    const int K = b.K, A = b.r + 1;
+    std::vector<int> ord((size_t)K * K);
+    LP_CUDA(cudaMemcpy(ord.data(), b.line_order, ord.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    std::vector<int> gp;
+    int prev_key = -1, run = 0;
+    for (size_t p = 0; p < ord.size(); ++p) {
+        const int key = ord[p] % K + A * (ord[p] / K);
+        if (key != prev_key || run == lpb) {
+            gp.push_back((int)p);
+            run = 0;
+            prev_key = key;
+        }
+        ++run;
+    }
+    gp.push_back((int)ord.size());
+    int rc = dalloc(&b.line_groups, gp.size(), "sweep line groups");
+    if (rc) return rc;
+    LP_CUDA(cudaMemcpyAsync(b.line_groups, gp.data(), gp.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    LP_CUDA(cudaStreamSynchronize(st));
+    b.n_line_groups = (int)gp.size() - 1;
+    return LP_OK;
+}
+
+static int small_reach_lpb(int r) {
+    switch (r) {
+        case 2: return S3m<2>::LPB;
+        case 3: return S3m<3>::LPB;
+        case 4: return S3m<4>::LPB;
+        default: return 0;
+    }
+}
+
 // The caller has pre-filled `out` with the sentinel and reset the ticket.
 int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket, cudaStream_t st) {
     Geom g = geom_of(m->box);
     if (!box_sweep3d_applies(g)) return LP_ERR_ARG;
     int rc = ensure_line_order(m->box, st);
     if (rc) return rc;
+    const int lpb = small_reach_lpb(g.r);
+    if (lpb && (rc = ensure_line_groups(m->box, lpb, st))) return rc;
     Sweep3Args a;
     a.g = g;
     a.lu = m->box.lu;
@@ -453,6 +772,8 @@ int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket
     a.out = out;
     a.ticket = ticket;
     a.order = m->box.line_order;
+    a.gpos = lpb ? m->box.line_groups : nullptr;
+    a.ngroups = lpb ? m->box.n_line_groups : g.nlines;
     a.nranks = 1;
     a.ys[0] = 0;
     a.ys[1] = g.K;

@@ -26,6 +26,8 @@ struct BoxLayout {
     double *band_lo = nullptr, *band_up = nullptr, *diag = nullptr;
     // 3-D sweeps: x-lines in wavefront order (see box_sweep3d.cu)
     int *line_order = nullptr;
+    int *line_groups = nullptr;   // small reach: starts of same-key groups in line_order
+    int n_line_groups = 0;
 };
 
 }  // namespace lp

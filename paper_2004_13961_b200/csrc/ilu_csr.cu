@@ -253,7 +253,8 @@ extern "C" int lp_ilu_destroy(lp_ilu *m) {
     cudaDeviceSynchronize();
     void *ptrs[] = {m->indptr, m->indices, m->values, m->lu, m->diag, m->flags, m->ticket,
                     m->bad, m->ytmp, m->box.values, m->box.lu, m->box.mask,
-                    m->box.band_lo, m->box.band_up, m->box.diag, m->box.line_order};
+                    m->box.band_lo, m->box.band_up, m->box.diag, m->box.line_order,
+                    m->box.line_groups};
     for (void *p : ptrs)
         if (p) dfree(p);
     delete m;

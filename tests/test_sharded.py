@@ -205,7 +205,7 @@ def test_cuda_stages_match_oracle():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,N,T,G", [("cfg4", 24, 8, 2), ("cfg4", 24, 8, 3), ("cfg5", 20, 3, 4),
-                                        ("cfg4", 40, 8, 4)])
+                                        ("cfg4", 40, 8, 4), ("cfg5", 24, 0, 3), ("cfg5", 20, 2, 2)])
 def test_rank_sweeps_bit_identical(name, N, T, G):
     """Sweeps over G y-slab ranks with halo publication == the one-rank sweeps."""
     from paper_2004_13961_b200 import TransformPlan, _lib
@@ -254,3 +254,21 @@ def test_sharded_pcg_matches_single_gpu(name, N, T, G):
         xo, ro = orc.pcg_solve(spec, F, epsilon=w.rtol, preconditioner=(T, T))
         assert abs(rg["iterations"] - ro["iterations"]) <= 1
         assert relerr(xg.cpu().numpy(), np.asarray(xo).flatten(order="F")) < 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,N,T", [("cfg5", 24, 0), ("cfg5", 20, 1), ("cfg4", 18, 2), ("cfg5", 16, 3),
+                                      ("cfg4", 14, 8)])
+def test_box_sweeps_match_csr_sweeps(name, N, T):
+    """The 3-D box sweeps (small-reach multi-line kernel for r <= 4, the line kernel
+    above) against the general CSR sweeps on the same factors."""
+    from paper_2004_13961_b200 import TransformPlan
+    from paper_2004_13961_b200.precond import assemble_M
+    from paper_2004_13961_b200.sparse import SparseMatrix, ilu0, precond_apply
+    w = wl.CONFIGS[name]()
+    m = assemble_M(spec_of(w, N), T, T, TransformPlan(N + 1))
+    csr = SparseMatrix(m.n, m.indptr, m.indices, m.values)
+    fb, fc = ilu0(m), ilu0(csr)
+    r = np.random.default_rng(9).standard_normal(m.n)
+    zb, zc = precond_apply(fb, r), precond_apply(fc, r)
+    assert relerr(zb, zc) < 1e-12
