@@ -384,7 +384,7 @@ struct S3m {
     static constexpr int LPB = NQP <= 16 ? 8 : 4;                      // lines per CTA
     static constexpr int NPW = LPB * NQP / 32;
     static constexpr int PPL = NQP > 32 ? NQP / 32 : 1;               // partial sums per line
-    static constexpr int NT = 32 * (NPW + 2);
+    static constexpr int NT = 32 * (NPW + 3);   // + loader, serial, watcher warps
     static constexpr int ROWD = (C + 1 + 1 + 1) / 2 * 2;
     static constexpr int NR = 6;
     static constexpr int P = W;   // window look-ahead (divides W)
@@ -445,37 +445,38 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
         };
 
         if (warp == 0) {
-            if (lane == 0) {
-                for (int u = 0; u < K; ++u) {
-                    const long long gs = gstep + u;
-                    const int slot = (int)(gs % NR);
-                    if (gs >= NR) {
-                        const int need = (int)(gs / NR) * (NPW + 1);
-                        const unsigned ca = smem_addr(&slotdone[slot]);
-                        int f;
-                        for (;;) {
-                            asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(f) : "r"(ca) : "memory");
-                            if (f >= need) break;
-                            __nanosleep(32);
-                        }
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            // ---------------- loader warp: lane j issues line j's copy
+            const int64_t lrow0 = lane < cnt ? (int64_t)line_of(lane) * K : 0;
+            for (int u = 0; u < K; ++u) {
+                const long long gs = gstep + u;
+                const int slot = (int)(gs % NR);
+                if (gs >= NR) {
+                    const int need = (int)(gs / NR) * (NPW + 1);
+                    const unsigned ca = smem_addr(&slotdone[slot]);
+                    int f;
+                    for (;;) {
+                        asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(f) : "r"(ca) : "memory");
+                        if (f >= need) break;
+                        __nanosleep(32);
                     }
-                    const int x = FWD ? u : K - 1 - u;
-                    unsigned total = 0;
-                    for (int j = 0; j < cnt; ++j) {
-                        const int64_t e0 = ((int64_t)line_of(j) * K + x) * S + base;
-                        total += (unsigned)(((e0 & 1) + len + 1) / 2 * 2) * 8;
-                    }
-                    mbar_expect(full_s + slot * 8, total);
-                    for (int j = 0; j < cnt; ++j) {
-                        const int64_t e0 = ((int64_t)line_of(j) * K + x) * S + base;
-                        const int64_t ea = e0 & ~(int64_t)1;
-                        const unsigned bytes = (unsigned)(((e0 - ea) + len + 1) / 2 * 2) * 8;
-                        bulk_g2s_hint(ring_s + (unsigned)((slot * LPB + j) * ROWD) * 8, a.lu + ea, bytes,
-                                      full_s + slot * 8, pol_stream);
-                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
-            } else if (lane == 1) {
+                const int x = FWD ? u : K - 1 - u;
+                const int64_t e0 = (lrow0 + x) * S + base;
+                const int64_t ea = e0 & ~(int64_t)1;
+                const unsigned bytes = lane < cnt ? (unsigned)(((e0 - ea) + len + 1) / 2 * 2) * 8 : 0u;
+                unsigned total = bytes;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+                if (lane == 0) mbar_expect(full_s + slot * 8, total);
+                __syncwarp();
+                if (lane < cnt)
+                    bulk_g2s_hint(ring_s + (unsigned)((slot * LPB + lane) * ROWD) * 8, a.lu + ea, bytes,
+                                  full_s + slot * 8, pol_stream);
+            }
+        } else if (warp == 2) {
+            // ---------------- watcher lane
+            if (lane == 0) {
                 for (int u = 0; u < K; ++u) {
                     const long long gs = gstep + u;
                     const int slot = (int)(gs % NR);
@@ -549,8 +550,7 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
             }
         } else {
             // ---------------- producers: lane (j, q) = source q of line j
-            const int p = tid - 64;
-            const int pw = warp - 2;
+            const int p = tid - 96;
             const int j = p / NQP, q = p % NQP;
             const int ql = FWD ? q : NQ + 1 + q;
             const int oy = ql % W - R, oz = ql / W - R;
@@ -563,14 +563,13 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
             auto fetch = [&](int pp) {
                 return (active && pp >= 0 && pp < K) ? ld_l2(srcp(pp), pol_keep) : 0.0;
             };
-            double win[W], yq[P3], yr = 0.0;
+            double win[W], yq[P3];   // loads P3 rows ahead; a sentinel is polled again when needed
 #pragma unroll
             for (int k = 0; k < W; ++k) win[k] = 0.0;
 #pragma unroll
             for (int pp = 0; pp < R; ++pp) win[pp % W] = fetch(pp);
 #pragma unroll
             for (int k = 0; k < P3; ++k) yq[k] = fetch(R + k);
-            yr = yq[0];
 #pragma unroll
             for (int pp = 0; pp < R; ++pp)
                 if (active && pp < K) win[pp % W] = wait_value(srcp(pp), win[pp % W]);
@@ -588,11 +587,9 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
                         {
                             const int pp = u + R;
                             double v = yq[k % P3];
-                            if (is_sent(v)) v = yr;
                             if (active && pp < K) v = wait_value(srcp(pp), v);
                             win[(k + R) % W] = v;
                             yq[k % P3] = fetch(pp + P3);
-                            yr = fetch(pp + 1);
                         }
                         wait_row(slot, gs);
                         double s0 = 0.0, s1 = 0.0;
