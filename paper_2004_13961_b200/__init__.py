@@ -5,7 +5,8 @@ PCG solver of arXiv:2004.13961, a drop-in for the reference package
 fallback.
 """
 
-from .coefficients import CoefficientField, LegendreSeriesField, constant_field, zero_field
+from .coefficients import (PRESETS, CoefficientField, LegendreSeriesField, constant_field, preset,
+                           zero_field)
 from .operator import (ProblemSpec, SpectralCoeffs, apply_A, apply_B, apply_system,
                        assemble_rhs)
 from .pcg import (IndefiniteOperatorError, SolveReport, SolverConfig, pcg_solve,
@@ -17,5 +18,6 @@ from .quadrature import (GaussRule, dphi_to_legendre, gauss_rule, legendre_table
 from .sparse import (IluFactors, IluZeroPivotError, SparseMatrix, backward_sub, forward_sub,
                      ilu0, precond_apply, spmv)
 from .transforms import TransformPlan, bdlt, fdlt, tensor_bdlt, tensor_fdlt
+from .benchmarks import BENCHMARKS, benchmark_rhs, make_problem, run_benchmark
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -20,7 +20,7 @@ from typing import Callable
 import numpy as np
 
 __all__ = ["CoefficientField", "LegendreSeriesField", "zero_field",
-           "constant_field"]
+           "constant_field", "PRESETS", "preset"]
 
 
 @dataclass(frozen=True)
@@ -95,3 +95,67 @@ class LegendreSeriesField(CoefficientField):
             tab = np.stack(_legendre_rows(x, self.hat.shape[a] - 1), axis=1)
             out = np.moveaxis(np.tensordot(tab, out, axes=([1], [a])), 0, a)
         return self.offset + out
+
+
+# --------------------------------------------------------------- presets
+# The paper's examples (Tables 7-10) as named coefficient presets, the
+# reference's `preset` / `PRESETS` contract (coefficients.py:53-127): a dict with
+# dim, beta, alpha and axis_betas (per-axis 1-D diffusion factors) per name.
+
+def _sq_norm(coords):
+    return sum(np.asarray(c, dtype=float) ** 2 for c in coords)
+
+
+def _quartic(*coords):            # (2|x|^2 + 1)^4
+    return (2.0 * _sq_norm(coords) + 1.0) ** 4
+
+
+def _exp_two_sum(*coords):        # e^{2(x + y + ...)}
+    return np.exp(2.0 * sum(np.asarray(c, dtype=float) for c in coords))
+
+
+def _cos_of_sum(*coords):         # cos(x + y + ...)
+    return np.cos(sum(np.asarray(c, dtype=float) for c in coords))
+
+
+_AXIS_FIELDS = {
+    "exp2x": (lambda x: np.exp(2.0 * x), "e^{2x}"),
+    "cosx": (np.cos, "cos(x)"),
+    "expx": (np.exp, "e^x"),
+    "cos_sin": (lambda x: np.cos(np.sin(x)), "cos(sin(x))"),
+    "runge100": (lambda x: 1.0 / (1.0 + 100.0 * x * x), "1/(1+100x^2)"),
+}
+
+
+def _axis_field(key):
+    fn, name = _AXIS_FIELDS[key]
+    return CoefficientField(1, fn, name=name)
+
+
+def _preset_table():
+    t = {}
+
+    def add(name, dim, beta=None, alpha=None, axis_betas=None):
+        t[name] = {"dim": dim, "beta": beta, "alpha": alpha, "axis_betas": axis_betas}
+
+    for d, tag in ((1, "1"), (2, "2"), (3, "3")):
+        add(f"example{tag}a", d, beta=CoefficientField(d, _quartic, name="(2|x|^2+1)^4"),
+            alpha=CoefficientField(d, _cos_of_sum, name="cos(sum x)"))
+        add(f"example{tag}b", d, beta=CoefficientField(d, _exp_two_sum, name="e^{2 sum x}"),
+            alpha=zero_field(d))
+    add("example4a", 2, alpha=zero_field(2), axis_betas=(_axis_field("exp2x"), _axis_field("cosx")))
+    add("example4b", 3, alpha=zero_field(3),
+        axis_betas=(_axis_field("exp2x"), _axis_field("cosx"), _axis_field("cosx")))
+    for key in ("expx", "cos_sin", "runge100"):     # 1-D rank-study fields
+        add(key, 1, beta=_axis_field(key), alpha=_axis_field(key))
+    return t
+
+
+PRESETS = _preset_table()
+
+
+def preset(name):
+    """Named coefficient preset; KeyError for unknown names (coefficients.py:122-127)."""
+    if name not in PRESETS:
+        raise KeyError(f"unknown coefficient preset {name!r}")
+    return PRESETS[name]
