@@ -20,7 +20,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib, device
-from .coefficients import CoefficientField
+from .coefficients import CoefficientField, LegendreSeriesField
 from .transforms import TransformPlan, tensor_fdlt
 
 __all__ = ["SpectralCoeffs", "ProblemSpec", "apply_A", "apply_B", "apply_system",
@@ -137,21 +137,58 @@ class ProblemSpec:
                 ptrs = (ctypes.c_void_p * d)(*[a.ctypes.data for a in arrs])
                 beta_ptr, nab = None, d
             else:
-                # x-fastest device order = transpose of the ij-indexed grid
-                g = np.ascontiguousarray(self.grid_values(plan, "beta").T)
+                g = _series_grid_on_device(self.beta, plan, d)
+                if g is None:
+                    # x-fastest device order = transpose of the ij-indexed grid
+                    g = np.ascontiguousarray(self.grid_values(plan, "beta").T)
+                    beta_ptr = g.ctypes.data
+                else:
+                    beta_ptr = g.data_ptr()
                 keep.append(g)
-                beta_ptr, nab, ptrs = g.ctypes.data, 0, None
+                nab, ptrs = 0, None
             alpha_ptr = None
             if self.has_reaction:
-                ga = np.ascontiguousarray(
-                    np.broadcast_to(self.grid_values(plan, "alpha"), (plan.order,) * d).T)
+                ga = _series_grid_on_device(self.alpha, plan, d)
+                if ga is None:
+                    ga = np.ascontiguousarray(
+                        np.broadcast_to(self.grid_values(plan, "alpha"), (plan.order,) * d).T)
+                    alpha_ptr = ga.ctypes.data
+                else:
+                    alpha_ptr = ga.data_ptr()
                 keep.append(ga)
-                alpha_ptr = ga.ctypes.data
             _lib.check(lib.lp_operator_create(plan.handle, d, beta_ptr, nab, ptrs, alpha_ptr,
                                               ctypes.byref(h)), "operator")
             self._op_cache[key] = (h.value, plan)
             weakref.finalize(self, _destroy_op, h.value)
+            if any(not isinstance(k, np.ndarray) for k in keep):
+                # device-built grids were copied into the operator: hand their
+                # memory back (the preconditioner of cfg 5 needs ~140 GB next)
+                del keep
+                device.torch().cuda.empty_cache()
         return self._op_cache[key][0]
+
+
+def _series_grid_on_device(fld, plan, d):
+    """Values of a truncated Legendre series field on the P^d Gauss grid, built on
+    the GPU: the tensor BDLT of the zero-padded hat, with the
+    offset folded into the L_0...L_0 coefficient.  This is the grid_values of
+    operator.py:95-120 for these fields (the series is exact at the nodes), without
+    the host P^d evaluation and upload (cfg 5: two 1.08 GB grids).  None for other
+    fields, which are user callables evaluated on the host."""
+    if not isinstance(fld, LegendreSeriesField) or fld.dim != d:
+        return None
+    P = plan.order
+    if any(s > P for s in fld.hat.shape):
+        return None
+    pad = np.zeros((P,) * d)
+    pad[tuple(slice(0, s) for s in fld.hat.shape)] = fld.hat
+    pad[(0,) * d] += fld.offset
+    src = device.to_device(pad.flatten(order="F"))      # x fastest
+    out = device.empty(P ** d)
+    _lib.check(_lib.load().lp_tensor_bdlt(plan.handle, d, src.data_ptr(), out.data_ptr(),
+                                          _lib.stream_ptr()), "series grid")
+    device.torch().cuda.current_stream().synchronize()
+    return out
 
 
 def _check_input(spec, plan, u):
