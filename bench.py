@@ -143,7 +143,7 @@ def dgemm_tflops(torch):
     return 2.0 * n ** 3 / best / 1e12
 
 
-PROFILE_TAG = "r01b"   # cfg-2 sweep/ILU/matvec captures (profiles/r01b_*_full.csv)
+PROFILE_TAG = "r01e"   # cfg-2 sweep/ILU/matvec captures (profiles/r01e_*_full.csv)
 
 
 def _ncu_rows(name):
