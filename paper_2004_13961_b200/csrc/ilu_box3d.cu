@@ -125,6 +125,12 @@ __device__ __forceinline__ double div_by_recip(double a, double b, double y) {
     return __fma_rn(r, y, q0);
 }
 
+#define LSTORE(idx, val)                                                                   \
+    do {                                                                                   \
+        const double _v = (val);                                                           \
+        *(volatile double *)(sh_l + ((idx) & 63)) = isnan(_v) ? __longlong_as_double(0x7FF8000000000000ll) : _v; \
+    } while (0)
+
 template <int R>
 __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __grid_constant__ Ilu3Args a) {
     using G = Cfg<R>;
@@ -135,7 +141,7 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
     double *spiv = stage + (size_t)D * G::STAGE;                        // [D]
     uint32_t *bits = reinterpret_cast<uint32_t *>(spiv + D);            // [mw]
     int *plist = reinterpret_cast<int *>(bits + a.g.mw);                // [C] packed pivots
-    __shared__ double sh_l[2];
+    __shared__ double sh_l[64];   // l of pivot en at en % 64; sentinel = not yet published
     __shared__ long long sh_i;
     __shared__ int sh_wcount[(C + 31) / 32 + 1];
     const int tid = threadIdx.x;
@@ -216,6 +222,7 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
 #pragma unroll
             for (int z = 0; z < W; ++z) colbits |= (unsigned)bit_of(bits, tid + z * W2) << z;
         }
+        if (tid < 64) sh_l[tid] = __longlong_as_double(0x7FF4000000000ABCll);
         __syncthreads();
         const int npiv = sh_wcount[NWL];
 
@@ -285,7 +292,7 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
                     const double piv = spiv[slot];
                     const double l = __ddiv_rn(v[pzi], piv);
                     v[pzi] = l;
-                    sh_l[en & 1] = l;
+                    LSTORE(en, l);
                     if (fabs(piv) < a.tol) {
                         const int64_t k = i + px + (int64_t)K * (py + (int64_t)K * (pzi - R));
                         atomicMin(a.bad, (unsigned long long)(i * n + k));
@@ -300,8 +307,21 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
                     piv1 = spiv[(en + 1) % D];
                     y1 = __drcp_rn(piv1);
                 }
-                __syncthreads();
-                const double l = sh_l[en & 1];
+                // no barrier per pivot: l is its own flag (sentinel-initialised
+                // ring), a barrier every 32 pivots bounds the warps' drift and
+                // recycles the half of the ring that every warp has consumed
+                if ((en & 31) == 0 && en > 0) {
+                    __syncthreads();
+                    if (tid < 32) sh_l[((en & 63) ^ 32) + tid] = __longlong_as_double(0x7FF4000000000ABCll);
+                    __syncthreads();
+                }
+                double l;
+                {
+                    const volatile double *lp = sh_l + (en & 63);
+                    do {
+                        l = *lp;
+                    } while (__double_as_longlong(l) == 0x7FF4000000000ABCll);
+                }
                 if (col && abs(tx - px) <= R && abs(ty - py) <= R) {
                     unsigned m = (colbits >> pzi) & ((1u << (R + 1)) - 1u);
                     if (!(ty > py || (ty == py && tx > px))) m &= ~1u;
@@ -311,7 +331,7 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
                     if (next_here && tid == own1) {
                         const double l1 = div_by_recip(v[pzi], piv1, y1);
                         v[pzi] = l1;
-                        sh_l[(en + 1) & 1] = l1;
+                        LSTORE(en + 1, l1);
                         if (fabs(piv1) < a.tol) {
                             const int px1 = ((e1 >> 14) & 31) - R, py1 = ((e1 >> 19) & 31) - R;
                             const int64_t k = i + px1 + (int64_t)K * (py1 + (int64_t)K * (pzi - R));
@@ -325,7 +345,7 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
                 } else if (next_here && tid == own1) {
                     const double l1 = div_by_recip(v[pzi], piv1, y1);
                     v[pzi] = l1;
-                    sh_l[(en + 1) & 1] = l1;
+                    LSTORE(en + 1, l1);
                     if (fabs(piv1) < a.tol) {
                         const int px1 = ((e1 >> 14) & 31) - R, py1 = ((e1 >> 19) & 31) - R;
                         const int64_t k = i + px1 + (int64_t)K * (py1 + (int64_t)K * (pzi - R));
