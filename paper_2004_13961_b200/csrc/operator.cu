@@ -292,6 +292,7 @@ extern "C" int lp_operator_destroy(lp_operator *op) {
     if (op->alpha_w) dfree(op->alpha_w);
     if (op->wsA) dfree(op->wsA);
     if (op->wsB) dfree(op->wsB);
+    if (op->slab_grid) dfree(op->slab_grid);
     delete op;
     return LP_OK;
 }

@@ -20,6 +20,10 @@ struct lp_operator {
     double *beta_w[3] = {nullptr, nullptr, nullptr};   // beta(x) w^d per diffusion direction
     double *alpha_w = nullptr;                         // alpha(x) w^d or null (B skipped)
     double *wsA = nullptr, *wsB = nullptr;             // 4 and 3 fields of P^d
+    // slab-sharded middle stage (slab.cu): the coefficient grids of one y' slab,
+    // [4][P][ny][P], extracted on first use
+    double *slab_grid = nullptr;
+    int slab_y0 = -1, slab_ny = -1;
 };
 
 namespace lp {

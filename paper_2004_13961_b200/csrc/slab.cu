@@ -118,22 +118,31 @@ extern "C" int lp_slab_middle(lp_operator *op, int which, int y0, int ny, const 
     const bool hasA = (which & 1) != 0;
     const bool hasB = (which & 2) != 0 && op->alpha_w != nullptr;
     const size_t nq = (size_t)P * ny * P;   // [z'][ny][x']
-    double *buf = nullptr;
-    LP_CUDA(cudaMallocAsync((void **)&buf, 8 * nq * sizeof(double), st));
-    double *q[4] = {buf, buf + nq, buf + 2 * nq, buf + 3 * nq};
-    double *gr[4] = {buf + 4 * nq, buf + 5 * nq, buf + 6 * nq, buf + 7 * nq};
-    int rc = LP_OK;
-    auto body = [&]() -> int {
-        // the coefficient grids of the slab, in the S3 output layout [z'][y' - y0][x']
+    // the coefficient grids of the slab, in the S3 output layout [z'][y' - y0][x'],
+    // extracted once per (operator, slab) and kept with the operator
+    if (op->slab_y0 != y0 || op->slab_ny != ny) {
+        if (op->slab_grid) dfree(op->slab_grid);
+        op->slab_grid = nullptr;
+        int rcg = dalloc(&op->slab_grid, 4 * nq, "slab grids");
+        if (rcg) return rcg;
         const double *src[4] = {op->beta_w[0], op->beta_w[1], op->beta_w[2], op->alpha_w};
         for (int g = 0; g < 4; ++g) {
-            if (!src[g] || (g < 3 && !hasA) || (g == 3 && !hasB)) continue;
+            if (!src[g]) continue;
             // P planes z', each a block of ny rows of P at row offset y0
             for (int z = 0; z < P; ++z)
-                if ((rc = copy2d(ny, P, src[g] + ((size_t)z * P + y0) * P, P, gr[g] + (size_t)z * ny * P,
-                                 P, st)))
-                    return rc;
+                if ((rcg = copy2d(ny, P, src[g] + ((size_t)z * P + y0) * P, P,
+                                  op->slab_grid + g * nq + (size_t)z * ny * P, P, st)))
+                    return rcg;
         }
+        op->slab_y0 = y0;
+        op->slab_ny = ny;
+    }
+    double *buf = nullptr;
+    LP_CUDA(cudaMallocAsync((void **)&buf, 4 * nq * sizeof(double), st));
+    double *q[4] = {buf, buf + nq, buf + 2 * nq, buf + 3 * nq};
+    double *gr[4] = {op->slab_grid, op->slab_grid + nq, op->slab_grid + 2 * nq, op->slab_grid + 3 * nq};
+    int rc = LP_OK;
+    auto body = [&]() -> int {
         LtArgs s3 = lt_unfold(F, P * ny);
         int o = 0, iq0 = -1, iq1 = -1, iq2 = -1, iq3 = -1;
         if (hasA) {
