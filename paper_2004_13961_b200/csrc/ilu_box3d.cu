@@ -37,7 +37,7 @@
 #include "ilu.cuh"
 
 #ifndef LP_ILU3_LEVEL_MAX_R
-#define LP_ILU3_LEVEL_MAX_R 6   // level order for reach <= this; natural order above (measured: r=2 11x faster, r=4 1.3x, r=7 equal, r=10 1.2x slower)
+#define LP_ILU3_LEVEL_MAX_R 8   // level order for reach <= this; natural order above (measured, barrier-free kernel: r=2 11x faster, r=4 1.3x, r=7 1.24x, r=10 1.19x slower)
 #endif
 
 namespace lp {
