@@ -19,6 +19,7 @@ struct BoxLayout {
     double *values = nullptr;         // original M            [n][S]
     double *lu = nullptr;             // ILU(0) factors         [n][S]
     uint32_t *mask = nullptr;         // in-pattern bits        [n][ceil(S/32)] (null: all valid slots)
+    unsigned char *full = nullptr;    // [n]: every slot of the row is in the pattern
     int mask_words = 0;
     int64_t nnz = 0;
     // compact in-line bands of the factors for the sweeps' serial recurrence:
@@ -28,6 +29,10 @@ struct BoxLayout {
     int *line_order = nullptr;
     int *line_groups = nullptr;   // small reach: starts of same-key groups in line_order
     int n_line_groups = 0;
+    // 2-D factorisation (ilu_box2d.cu): block tasks in key order, RN(1/u_ii) per row
+    int *ilu_tasks = nullptr;
+    int ilu_ntask = 0, ilu_nb = 0;
+    double *rdiag = nullptr;          // [n][2]
 };
 
 }  // namespace lp
@@ -66,8 +71,8 @@ int box_spmv(lp_ilu *m, const double *x, double *y, cudaStream_t st);
 int box_export(const lp_ilu *m, int which, int64_t *indptr, int32_t *indices, double *values);
 int box_build_bands(lp_ilu *m, cudaStream_t st);
 int box_apply(lp_ilu *m, const double *r, double *z, cudaStream_t st);
-int box_ilu0_2d_tasks(lp_ilu *m, double tol, unsigned long long *key, const unsigned char *full,
-                      int *edone, cudaStream_t st);
+int box_ilu0_2d_tasks(lp_ilu *m, const double *src, double tol, unsigned long long *key, int *done,
+                      cudaStream_t st);
 int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_t st);
 struct Geom;
 bool box_sweep3d_applies(const Geom &g);

@@ -127,6 +127,115 @@ __global__ void box_mask_kernel(Geom g, double *vals, uint32_t *mask,
     if (lane == 0 && cnt) atomicAdd(nnz, cnt);
 }
 
+// Fused assembly (raw products, pattern, nnz and the full-row flags in one
+// pass over M).  The raw entry of (row, slot) is
+//   sum_g sum_t H_g[t](line, slot-line) X_t[ox](ix),  H_g[t] = sum_{b,c} hat_g[t,b,c] Y_b[oy](iy) Z_c[oz](iz),
+// and the 1-D block diagonals are stored mirrored exactly (building_blocks_1d),
+// so entry (j, i) is evaluated from bitwise the same operands in the same order
+// as entry (i, j): the raw M is exactly symmetric and the averaging of
+// precond.py:255-269 returns every value unchanged (0.5 (v + v) = v).  The
+// separate symmetrisation pass is therefore not needed.
+// CTA = (x-line, chunk of ASM_RB rows); H of every slot-line of the line in
+// shared memory; warp = row, lane = x offset, looping over the slot-lines, so
+// each store is a run of W contiguous doubles and the row's pattern bits are
+// built by ballots in warp-private shared memory.
+constexpr int ASM_RB = 32;
+constexpr int ASM_MAXJ = 8;   // parity-matched degrees per group in registers (tmax <= 15)
+
+__global__ void __launch_bounds__(256)
+box_assemble_kernel(const __grid_constant__ AsmArgs a, double *__restrict__ vals,
+                    uint32_t *__restrict__ mask, unsigned char *__restrict__ full,
+                    unsigned long long *nnz, unsigned long long *missing) {
+    extern __shared__ __align__(16) double sm[];
+    const Geom &g = a.g;
+    const int nsl = g.d == 1 ? 1 : (g.d == 2 ? g.W : g.W * g.W);
+    const int TL = a.tmax + 1, NG = a.ngroups;
+    double *H = sm;   // [nsl][NG][TL]
+    uint32_t *mk = reinterpret_cast<uint32_t *>(H + (size_t)nsl * NG * TL);   // [ASM_RB][mw]
+    const int line = blockIdx.x;
+    const int iy = g.d > 1 ? line % g.K : 0, iz = g.d > 2 ? line / g.K : 0;
+    const int x0 = blockIdx.y * ASM_RB;
+    const int nrows = min(ASM_RB, g.K - x0);
+    for (int q = threadIdx.x; q < nsl * NG * TL; q += blockDim.x) {
+        const int t = q % TL, gi = (q / TL) % NG, sl = q / (TL * NG);
+        const int oy = g.d > 1 ? sl % g.W - g.r : 0, oz = g.d > 2 ? sl / g.W - g.r : 0;
+        const GroupDesc &G = a.grp[gi];
+        double h = 0.0;
+        if (t < G.lens[0]) {
+            const int ly = G.lens[1], lz = G.lens[2];
+            for (int b = (oy & 1); b < ly; b += 2) {
+                const double yb = g.d > 1 ? blk(a, G.kind[1], b, oy, iy) : 1.0;
+                for (int c = (oz & 1); c < lz; c += 2) {
+                    const double zc = g.d > 2 ? blk(a, G.kind[2], c, oz, iz) : 1.0;
+                    h += a.hats[G.hat_off + ((size_t)t * ly + b) * lz + c] * yb * zc;
+                }
+            }
+        }
+        H[q] = h;
+    }
+    for (int q = threadIdx.x; q < nrows * g.mw; q += blockDim.x) mk[q] = 0u;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ox = lane - g.r;
+    const bool xlane = lane < g.W;
+    unsigned long long cnt = 0;
+    for (int rl = warp; rl < nrows; rl += blockDim.x >> 5) {
+        const int ix = x0 + rl;
+        const int64_t i = (int64_t)line * g.K + ix;
+        double xr[4][ASM_MAXJ];
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi)
+#pragma unroll
+            for (int j = 0; j < ASM_MAXJ; ++j) {
+                const int t = (ox & 1) + 2 * j;
+                xr[gi][j] = (gi < NG && xlane && t < a.grp[gi].lens[0])
+                                ? blk(a, a.grp[gi].kind[0], t, ox, ix) : 0.0;
+            }
+        const bool xok = xlane && ix + ox >= 0 && ix + ox < g.K;
+        uint32_t *mrow = mk + rl * g.mw;
+        double *vrow = vals + (size_t)i * g.S;
+        for (int sl = 0; sl < nsl; ++sl) {
+            const int oy = g.d > 1 ? sl % g.W - g.r : 0, oz = g.d > 2 ? sl / g.W - g.r : 0;
+            const bool ok = xok && (g.d < 2 || (iy + oy >= 0 && iy + oy < g.K)) &&
+                            (g.d < 3 || (iz + oz >= 0 && iz + oz < g.K));
+            const double *Hs = H + (size_t)sl * NG * TL;
+            double v = 0.0;
+#pragma unroll
+            for (int gi = 0; gi < 4; ++gi) {
+                if (gi >= NG) break;
+                const int L0 = a.grp[gi].lens[0];
+#pragma unroll
+                for (int j = 0; j < ASM_MAXJ; ++j) {
+                    const int t = (ox & 1) + 2 * j;
+                    if (t < L0) v += Hs[gi * TL + t] * xr[gi][j];
+                }
+            }
+            const bool in = ok && fabs(v) >= 1e-300;
+            if (xlane) vrow[sl * g.W + lane] = in ? v : 0.0;
+            const unsigned bits = __ballot_sync(0xffffffffu, in);
+            if (lane == 0 && bits) {
+                const int s0 = sl * g.W, w0 = s0 >> 5, sh = s0 & 31;
+                mrow[w0] |= bits << sh;
+                if (sh && (bits >> (32 - sh))) mrow[w0 + 1] |= bits >> (32 - sh);
+            }
+        }
+        __syncwarp();
+        int pc = 0;
+        for (int w = lane; w < g.mw; w += 32) pc += __popc(mrow[w]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, o);
+        if (lane == 0) {
+            full[i] = pc == g.S;
+            cnt += (unsigned long long)pc;
+            if (!((mrow[g.c >> 5] >> (g.c & 31)) & 1u)) atomicMin(missing, (unsigned long long)i);
+        }
+    }
+    if (lane == 0 && cnt) atomicAdd(nnz, cnt);
+    __syncthreads();
+    uint32_t *mdst = mask + ((size_t)line * g.K + x0) * g.mw;
+    for (int q = threadIdx.x; q < nrows * g.mw; q += blockDim.x) mdst[q] = mk[q];
+}
+
 // full[i] = 1 when every slot of row i is in the pattern (interior rows of a
 // full box): the factorisation then needs no boundary or pattern checks.
 __global__ void box_full_kernel(Geom g, const uint32_t *__restrict__ mask,
@@ -484,11 +593,14 @@ int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st) {
             b.values = nullptr;
         }
     }
-    if (b.values) LP_CUDA(cudaMemcpyAsync(b.lu, b.values, bytes, cudaMemcpyDeviceToDevice, st));
-    else if (m->factored) {
+    if (!b.values && m->factored) {
         set_error("matrix was factored in place; re-assemble before refactoring");
         return LP_ERR_ARG;
     }
+    // the 2-D block-wavefront kernel reads M and writes the factors itself; the
+    // other kernels factor a copy in place
+    const bool wave2d = g.d == 2 && g.r >= 1 && g.r <= 14 && b.full;
+    if (b.values && !wave2d) LP_CUDA(cudaMemcpyAsync(b.lu, b.values, bytes, cudaMemcpyDeviceToDevice, st));
     unsigned long long *key = reinterpret_cast<unsigned long long *>(m->bad);
     const unsigned long long none = ~0ull;
     LP_CUDA(cudaMemcpyAsync(key, &none, sizeof none, cudaMemcpyHostToDevice, st));
@@ -511,24 +623,18 @@ int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st) {
     // 198 ms; cfg 3, K (r+1) = 30705 -> row kernel 9.5 s vs line kernel 3.1 s.)
     const bool window_ok = (int64_t)g.K * (g.r + 1) <= 8192;
     bool done = false;
-    if (g.d == 2) {
-        // task-graph factorisation (ilu_box2d.cu)
-        unsigned char *full = nullptr;
-        int *edone = nullptr;
-        const int nb = (g.K + 15) / 16;
+    if (wave2d) {
+        // block-wavefront factorisation (ilu_box2d.cu)
+        int *bdone = nullptr;
+        const int nb = (g.K + 13) / 14;
         int rcf;
-        if ((rcf = dalloc(&full, (size_t)b.n, "full-row flags"))) return rcf;
-        if ((rcf = dalloc(&edone, (size_t)g.nlines * nb, "task flags"))) return rcf;
-        LP_CUDA(cudaMemsetAsync(edone, 0, (size_t)g.nlines * nb * sizeof(int), st));
-        box_full_kernel<<<148 * 8, 256, 0, st>>>(g, b.mask, full);
-        count_launch();
-        const int rt = box_ilu0_2d_tasks(m, tol, key, full, edone, st);
-        if (rt == LP_OK) {
-            LP_CUDA(cudaStreamSynchronize(st));
-            done = true;
-        }
-        dfree(full);
-        dfree(edone);
+        if ((rcf = dalloc(&bdone, (size_t)g.nlines * nb, "block flags"))) return rcf;
+        LP_CUDA(cudaMemsetAsync(bdone, 0, (size_t)g.nlines * nb * sizeof(int), st));
+        const int rt = box_ilu0_2d_tasks(m, b.values ? b.values : b.lu, tol, key, bdone, st);
+        dfree(bdone);
+        if (rt != LP_OK) return rt;
+        LP_CUDA(cudaStreamSynchronize(st));
+        done = true;
     }
     if (g.d == 3 && b.mask) {
         // row-per-CTA kernel (ilu_box3d.cu)
@@ -544,15 +650,10 @@ int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st) {
                                                               32 * LNW, line_smem));
         int64_t blocks = (int64_t)occ * nsm;
         if (blocks > g.nlines) blocks = g.nlines;
-        unsigned char *full = nullptr;
-        int rcf;
-        if ((rcf = dalloc(&full, (size_t)b.n, "full-row flags"))) return rcf;
-        box_full_kernel<<<148 * 8, 256, 0, st>>>(g, b.mask, full);
         box_ilu0_line_kernel<LNW><<<(unsigned)blocks, 32 * LNW, line_smem, st>>>(
-            g, b.lu, b.mask, full, m->flags, epoch, m->ticket, tol, key);
+            g, b.lu, b.mask, b.full, m->flags, epoch, m->ticket, tol, key);
         count_launch();
         LP_CUDA(cudaStreamSynchronize(st));
-        dfree(full);
     } else if (g.S <= 1200) {
         LP_CUDA(cudaFuncSetAttribute(box_ilu0_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
@@ -710,10 +811,24 @@ extern "C" int lp_box_assemble(int d, int K, int n_groups, const int *lens, cons
     if (e != cudaSuccess) return fail(cuda_fail(e, "counter init", __FILE__, __LINE__));
     const int wd = d > 1 ? b.W : 1;
     const unsigned slot_lines = (unsigned)(d > 2 ? wd * wd : wd);
-    box_raw_kernel<<<dim3((unsigned)a.g.nlines, slot_lines), 128>>>(a, b.values);
-    box_sym_kernel<<<148 * 8, 256>>>(a.g, b.values);
-    box_mask_kernel<<<148 * 8, 256>>>(a.g, b.values, b.mask, cnt, cnt + 1);
-    count_launch(3);
+    const size_t asm_smem = (size_t)slot_lines * n_groups * (tmax + 1) * sizeof(double) +
+                            (size_t)ASM_RB * b.mask_words * sizeof(uint32_t);
+    if ((rc = dalloc(&b.full, (size_t)b.n, "full-row flags"))) return fail(rc);
+    if (b.W <= 32 && tmax + 1 <= 2 * ASM_MAXJ && asm_smem <= 200 * 1024) {
+        e = cudaFuncSetAttribute(box_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)asm_smem);
+        if (e != cudaSuccess) return fail(cuda_fail(e, "assembly attribute", __FILE__, __LINE__));
+        box_assemble_kernel<<<dim3((unsigned)a.g.nlines, (unsigned)ceil_div(K, ASM_RB)), 256,
+                              asm_smem>>>(a, b.values, b.mask, b.full, cnt, cnt + 1);
+        count_launch(1);
+    } else {
+        // general reach / degree: raw products, symmetrisation, pattern (three passes)
+        box_raw_kernel<<<dim3((unsigned)a.g.nlines, slot_lines), 128>>>(a, b.values);
+        box_sym_kernel<<<148 * 8, 256>>>(a.g, b.values);
+        box_mask_kernel<<<148 * 8, 256>>>(a.g, b.values, b.mask, cnt, cnt + 1);
+        box_full_kernel<<<148 * 8, 256>>>(a.g, b.mask, b.full);
+        count_launch(4);
+    }
     unsigned long long host[2];
     e = cudaMemcpy(host, cnt, sizeof host, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail(cuda_fail(e, "assembly", __FILE__, __LINE__));

@@ -1,406 +1,506 @@
-// ILU(0) of a 2-D box matrix as a task graph on a persistent grid.
+// ILU(0) of a 2-D box matrix (sparse.py:116-139) as a key-ordered block
+// wavefront with register-resident rows.
 //
-// IKJ elimination (sparse.py:116-139) of row i = (y, x) visits its lower slots in
-// column order: first the rows of lines y-r..y-1, then the in-line rows x-r..x-1.
-// Every entry receives its updates in that order, each a separately rounded
-// multiply and subtract, so any schedule that keeps the per-entry k order yields
-// the reference's factors bit for bit.  The work splits into
+// IKJ elimination of row i = (x, y) visits its lower slots in column order:
+// the rows of lines y-r .. y-1 (x-r .. x+r each), then the in-line rows
+// x-r .. x-1.  Every entry receives its updates in that order, each a
+// separately rounded multiply and subtract, and every multiplier is the
+// correctly rounded quotient, so any schedule that keeps the per-entry k order
+// gives the reference's factors bit for bit.
 //
-//  * block tasks E(y, b): rows x in [16b, 16b+16) of line y eliminated against
-//    lines y-r..y-1 -- about 95% of the arithmetic, one warp per row.  Most of
-//    it uses lines that finished long ago, so these tasks run in parallel on
-//    many SMs; the pivot rows' upper parts stream through a shared-memory ring
-//    (TMA bulk copies), shared by the 16 rows of the task;
-//  * line tasks L(y): one CTA walks line y and finishes every row with its r
-//    in-line pivots, the sequential part; rows are taken round-robin by 16 warps
-//    and the pivots are read from the sibling warps' shared-memory buffers.
-//
-// One pivot application ("apply") is a shifted axpy over slot ranges: the
-// targets of pivot k = (ox, oy) are the offsets (tx, ty) with ty in
-// [oy, oy + r], |tx - ox| <= r, past k itself, and the pivot entry of target t
-// is slot t - s + c.  Interior rows have every slot in the pattern and skip the
-// mask; out-of-pattern pivot entries are stored zeros.
-//
-// Tasks are handed out by one ticket in the order L(0), E(1, *), L(1), E(2, *),
-// L(2), ...; a task only waits on tasks with smaller tickets, all held by
-// resident CTAs, so the grid cannot deadlock.  Completion is published per row
-// (values stored and fenced, then a flag) and per block task.
+// Task = block (y, b): rows x in [14 b, 14 b + 14) of line y, one CTA, 7
+// consumer warps with two adjacent rows each plus one loader warp.
+//  * A warp keeps its rows A = (x, y), B = (x+1, y) in registers: lane L owns
+//    the absolute column x - r + L, and holds that column's 2r+1 entries (all
+//    lines) of both rows.  A pivot row's entry at that column is then used by
+//    both rows from one shared-memory load, and the targets need no loads or
+//    stores at all: per update one DMUL + one DSUB.
+//  * E part: the pivots of lines y-r .. y-1 (x0-r .. x0+13+r each) stream
+//    through a 16-slot shared-memory ring by TMA bulk copies (the pivot row's
+//    diagonal and upper half, plus RN(1/u_kk)), issued by the loader warp; the
+//    consumers wait on the slot's mbarrier and report progress so the loader
+//    can reuse the slot.
+//  * In-line part: rows x-r .. x-1 of the same line, from the previous block
+//    (loaded into a line buffer by the loader once that block is published) or
+//    from the sibling warps (written to the line buffer as soon as final).
+//    Row B applies row A straight from registers (same lane = same column).
+//  * Quotients: Markstein's correction q = RN(q0 + RN(a - b q0) y) with
+//    y = RN(1/b) and q0 = RN(a y) is the correctly rounded a / b (no overflow
+//    or underflow); y is computed once per row by the row's owner and published
+//    with it.
+//  * Tasks go out by one ticket in key order key = b + 2y.  Block (y, b) needs
+//    blocks (y, b-1) (in-line rows) and (y-d, b-1 .. b+1), d = 1..r (pivot
+//    rows, r <= 14 = rows per block), all of smaller key: a task only waits on
+//    tasks held by resident CTAs, so the grid cannot deadlock, and the
+//    resident tasks of one key span many lines.  A block is published (row
+//    values stored, fence, release flag) when all its rows are final.
 #include <math.h>
+
+#include <vector>
 
 #include "box_geom.cuh"
 #include "ilu.cuh"
 #include "smem_tma.cuh"
 
 namespace lp {
-
-unsigned long long *g_ilu_trace = nullptr;   // LP_ILU_TRACE builds
-size_t g_ilu_trace_n = 0;
-
 namespace {
 
-constexpr int NW = 16;   // warps per CTA; early-task rows; line-task rows in flight
-constexpr int NR = 8;    // pivot-row ring slots of the early tasks
+constexpr int NWC = 7;                 // consumer warps, two rows each (8 warps: 255 registers)
+constexpr int RB = 2 * NWC;            // rows per block task
+constexpr int NRING = 16;              // pivot-row ring slots
+constexpr int NTHR = 32 * (NWC + 1);   // + the loader warp
+constexpr unsigned FULLM = 0xffffffffu;
 
-__device__ __forceinline__ int ld_flag(const int *p) {
-    int v;
-    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 
-__device__ __forceinline__ unsigned long long gtime_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-// Apply pivot row uk (uk[c] = pivot, uk[slot] its upper entries) at offset
-// (ox, oy) to the target row buffer `row` (slot s = the pivot's slot in the
-// row); returns l = row[s] / pivot (the caller stores it into row[s]).  Lane m
-// owns target column tx = max(-r, ox - r) + m and walks the target lines
-// oy .. oy + r; colmask[tx + r] has bit ty + r set when slot (tx, ty) is in
-// the row's pattern (interior rows: FULL, no mask).  All loads are issued
-// before any arithmetic (clamped indices, predicated stores): the warp is
-// latency bound, so one shared-memory round trip per pivot instead of 16.
-template <bool FULL, int R>
-__device__ __forceinline__ double apply_pivot(double *row, const uint32_t *colmask, const double *uk,
-                                              int s, int ox, int oy, int r, int W, int S, int c,
-                                              int lane) {
-    // R = r when specialised (every index below is in range, loads use immediate
-    // offsets); R = 0 for the generic path (clamped indices, up to 16 lines)
-    constexpr int MJ = R > 0 ? R + 1 : 16;
-    const int txlo = max(-r, ox - r), txhi = min(r, ox + r);
-    const int tx = txlo + lane;
-    const bool act = tx <= txhi;
-    const int nty = min(r, oy + r) - oy + 1;   // r + 1: pivots have oy <= 0
-    unsigned jm = (nty >= 32 ? ~0u : (1u << nty) - 1u);
-    if (tx <= ox) jm &= ~1u;
-    if (!act) jm = 0;
-    else if (!FULL) jm &= colmask[tx + r] >> (oy + r);
-    const int t0 = act ? (tx + r) + W * (oy + r) : r;
-    const int d = act ? c - s : 0;
-    double u[MJ], v[MJ];
-#pragma unroll
-    for (int j = 0; j < MJ; ++j) {
-        const int t = R > 0 ? t0 + W * j : min(t0 + W * j, S - 1);
-        u[j] = uk[R > 0 ? t + d : min(t + d, S - 1)];
-        v[j] = row[t];
-    }
-    const double l = __ddiv_rn(row[s], uk[c]);
-#pragma unroll
-    for (int j = 0; j < MJ; ++j)
-        if ((jm >> j) & 1u) row[t0 + W * j] = __dsub_rn(v[j], __dmul_rn(l, u[j]));
-    __syncwarp();
-    return l;
-}
-
-// colmask[tx] (tx = 0..W-1): bit ty set when slot tx + W ty is in the pattern.
-__device__ __forceinline__ void build_colmask(const uint32_t *bits, uint32_t *colmask, int W, int lane) {
-    if (lane < W) {
-        uint32_t m = 0;
-        for (int ty = 0; ty < W; ++ty) {
-            const int t = lane + W * ty;
-            m |= ((bits[t >> 5] >> (t & 31)) & 1u) << ty;
-        }
-        colmask[lane] = m;
-    }
-}
-
-struct TaskArgs {
-    Geom g;
-    double *lu;
+struct Args {
+    int K, nlines, nb, ntask, epoch, mw;
+    int64_t n;
+    const double *src;            // M (each row read once by its owner; may equal lu)
+    double *lu;                   // factors [n][S]
+    double *rd;                   // [n][2]: RN(1/u_ii), 0
     const uint32_t *mask;
     const unsigned char *full;
-    int *rowf;     // [n]: row final (its values stored and fenced)
-    int *edone;    // [nlines][nb]: early task finished
+    const int *tasks;             // [ntask]: y * nb + b in key order
+    int *done;                    // [nlines][nb]: block published (== epoch)
     int *ticket;
     double tol;
     unsigned long long *bad;
-    int nb;        // early tasks per line
-    int rs;        // ring row stride (doubles)
-    int ntask;
-    unsigned long long *trace;   // LP_ILU_TRACE builds: [task][4] timestamps
 };
 
+__device__ __forceinline__ int ld_acq_gpu(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel_gpu(int *p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acq_cta(const int *p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel_cta(int *p, int v) {
+    asm volatile("st.release.cta.shared::cta.s32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_vol_cta(const int *p) {
+    int v;
+    asm volatile("ld.volatile.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_vol_cta(int *p, int v) {
+    asm volatile("st.volatile.shared::cta.s32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
+
+// correctly rounded a / b from y = RN(1/b) (Markstein)
+__device__ __forceinline__ double qdiv(double a, double b, double y) {
+    const double q0 = __dmul_rn(a, y);
+    const double rr = __fma_rn(-b, q0, a);
+    return __fma_rn(rr, y, q0);
+}
+
+// bits j (j < W) of the pattern of row i at relative column tx: slot tx + W j
+template <int W>
+__device__ __forceinline__ unsigned colbits(const uint32_t *mrow, int tx) {
+    unsigned m = 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        const int s = tx + W * j;
+        m |= ((__ldg(mrow + (s >> 5)) >> (s & 31)) & 1u) << j;
+    }
+    return m;
+}
+
+// One pivot application to the warp's two rows.  j0 (static): the pivot's
+// line relative to the rows (j0 = oy + r); Lk: lane of the pivot's column;
+// up[0] = u_kk, up[dx + W dy] = its upper entries; rc = RN(1/u_kk).
 template <int R>
-__global__ void __launch_bounds__(32 * NW, 1) box_ilu0_tasks(const __grid_constant__ TaskArgs a) {
-    extern __shared__ __align__(16) double sm[];
-    __shared__ __align__(8) unsigned long long s_full[NR];
-    __shared__ unsigned s_cons[NR];
-    __shared__ int s_rowdone[2 * NW];
-    __shared__ int s_task;
-    volatile unsigned *v_cons = s_cons;
-    volatile int *v_done = s_rowdone;
-    const Geom &g = a.g;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int K = g.K, r = g.r, W = g.W, S = g.S, c = g.c;
-    const int mwS = (g.mw + 1) & ~1;          // mask words, padded to 8 bytes
-    const int bufd = S + mwS / 2 + 16;        // doubles per row buffer: values, mask bits, column masks
-    if (tid == 0) {
-        for (int i = 0; i < NR; ++i) {
-            mbar_init(smem_addr(s_full + i), 1);
-            s_cons[i] = 0;
+__device__ __forceinline__ void apply2(double (&vA)[2 * R + 1], double (&vB)[2 * R + 1],
+                                       unsigned cmA, unsigned cmB, bool useA, bool useB, int j0,
+                                       int Lk, const double *up, double rc, int lane,
+                                       const Args &a, int64_t iA, int64_t k) {
+    constexpr int W = 2 * R + 1;
+    const int dx = lane - Lk;
+    const bool inp = dx >= -R && dx <= R;
+    double u[R + 1];
+#pragma unroll
+    for (int dy = 0; dy <= R; ++dy) u[dy] = (inp && (dy > 0 || dx > 0)) ? up[dx + W * dy] : 0.0;
+    const double upiv = up[0];
+    double aA = 0.0, aB = 0.0;
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+        if (j == j0) {
+            aA = __shfl_sync(FULLM, vA[j], Lk & 31);
+            aB = __shfl_sync(FULLM, vB[j], Lk & 31);
         }
+    const double lA = qdiv(aA, upiv, rc), lB = qdiv(aB, upiv, rc);
+    if (lane == 0 && fabs(upiv) < a.tol) {
+        if (useA) atomicMin(a.bad, (unsigned long long)(iA * a.n + k));
+        if (useB) atomicMin(a.bad, (unsigned long long)((iA + 1) * a.n + k));
+    }
+#pragma unroll
+    for (int dy = 0; dy <= R; ++dy) {
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (j == j0 + dy) {
+                const bool ok = inp && (dy > 0 || dx > 0);
+                if (useA && ok && ((cmA >> j) & 1u)) vA[j] = __dsub_rn(vA[j], __dmul_rn(lA, u[dy]));
+                if (useB && ok && ((cmB >> j) & 1u)) vB[j] = __dsub_rn(vB[j], __dmul_rn(lB, u[dy]));
+            }
+    }
+    if (lane == Lk) {
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (j == j0) {
+                if (useA) vA[j] = lA;
+                if (useB) vB[j] = lB;
+            }
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(NTHR, 1) ilu2d_kernel(const __grid_constant__ Args a) {
+    constexpr int W = 2 * R + 1, S = W * W, C = (S - 1) / 2;
+    constexpr int US = ((S - C + 1) + 1) & ~1;   // ring slot: diag + upper half (+ alignment)
+    constexpr int LS = ((S - C + R) + 1) & ~1;   // line-buffer slot: from slot C - R
+    constexpr int NL = R + RB;                   // line-buffer rows x0 - R .. x0 + RB - 1
+    extern __shared__ __align__(128) double sm[];
+    double *ring = sm;                           // [NRING][US]
+    double *rdr = ring + NRING * US;             // [NRING][2]
+    double *lbuf = rdr + 2 * NRING;              // [NL][LS]
+    double *rcl = lbuf + NL * LS;                // [NL]
+    __shared__ __align__(8) unsigned long long mbar[NRING];
+    __shared__ int s_lready[NL];
+    __shared__ int s_prog[NWC];
+    __shared__ int s_task;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int K = a.K;
+    const unsigned mbar0 = smem_addr(mbar);
+    if (tid == 0) {
+        for (int i = 0; i < NRING; ++i) mbar_init(mbar0 + 8 * i, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    unsigned kbase = 0;   // pivot rows this CTA has streamed (ring slot / phase)
+    for (int i = tid; i < NL; i += NTHR) s_lready[i] = -1;
+    if (tid < NWC) s_prog[tid] = 0;
+    unsigned gbase = 0;   // ring sequence number of the task's first pivot
     for (;;) {
         __syncthreads();
         if (tid == 0) s_task = atomicAdd(a.ticket, 1);
-        for (int q = tid; q < 2 * NW; q += blockDim.x) s_rowdone[q] = -1;
         __syncthreads();
         const int task = s_task;
         if (task >= a.ntask) return;
-        int y, b;   // b < 0: line task
-        if (task == 0) {
-            y = 0;
-            b = -1;
-        } else {
-            const int u = task - 1;
-            y = 1 + u / (a.nb + 1);
-            b = u % (a.nb + 1);
-            if (b == a.nb) b = -1;
-        }
-        const int64_t row0 = (int64_t)y * K;
+        const int yb = a.tasks[task];
+        const int y = yb / a.nb, b = yb - y * a.nb;
+        const int x0 = b * RB;
+        const int ylo = y > R ? y - R : 0;
+        const int xlo = max(0, x0 - R), xhi = min(K - 1, x0 + RB - 1 + R);
+        const int nx = xhi - xlo + 1;
+        const int nk = (y - ylo) * nx;
 
-        if (b >= 0) {
-            // ------------------------------------------------ block task E(y, b)
-#ifdef LP_ILU_TRACE
-            if (tid == 0 && a.trace) a.trace[(size_t)task * 8] = gtime_ns();
-#endif
-            const int x0 = NW * b;
-            const int x = x0 + warp;
-            const bool live = x < K;
-            const int64_t i = row0 + x;
-            double *row = sm + (size_t)warp * bufd;
-            uint32_t *bits = reinterpret_cast<uint32_t *>(row + S);
-            bool full_row = false;
-            uint32_t *colmask = bits + mwS;
-            if (live) {
-                for (int q = lane; q < S; q += 32) row[q] = a.lu[(size_t)i * S + q];
-                for (int q = lane; q < g.mw; q += 32) bits[q] = a.mask[(size_t)i * g.mw + q];
-                full_row = __ldg(a.full + i) != 0;
-                __syncwarp();
-                build_colmask(bits, colmask, W, lane);
+        if (warp == NWC) {
+            // ------------------------------------------------------------ loader
+            // pivot blocks of lines ylo..y-1 (b-1..b+1): one parallel round of
+            // acquire loads first, then lane 0 re-polls only the blocks not yet done
+            const int bl = max(0, b - 1), bh = min(a.nb - 1, (xhi) / RB);
+            const int nbk = bh - bl + 1;
+            const int nchk = (y - ylo) * nbk;   // <= 3 R <= 45
+            unsigned long long dmask = 0;
+            for (int q0 = 0; q0 < nchk; q0 += 32) {
+                const int q = q0 + lane;
+                bool ok = false;
+                if (q < nchk) ok = ld_acq_gpu(a.done + (ylo + q / nbk) * a.nb + bl + q % nbk) == a.epoch;
+                dmask |= (unsigned long long)__ballot_sync(FULLM, ok) << q0;
             }
-            __syncwarp();
-            const unsigned ring0 = smem_addr(sm + (size_t)NW * bufd);
-            const unsigned full0 = smem_addr(s_full);
-            const int ylo = max(0, y - r), yhi = y - 1;   // pivot lines
-            const int xlo = max(0, x0 - r), xhi = min(K - 1, x0 + NW - 1 + r);
-            const int nx = xhi - xlo + 1;
-            const int nk = (yhi - ylo + 1) * nx;
-            const int ncopy = S - c;                     // diag + upper slots of a pivot row
-            int qi = 0;                                  // next pivot to stream (warp 0)
-            auto issue = [&](int q) {
-                const int yk = ylo + q / nx, xk = xlo + q % nx;
-                const unsigned G = kbase + (unsigned)q, slot = G % NR;
-                if (lane == 0) {
-                    while (v_cons[slot] < NW * (G / NR)) __nanosleep(32);
-                    while (ld_flag(a.rowf + (int64_t)yk * K + xk) == 0) __nanosleep(64);
-#ifdef LP_ILU_TRACE
-                    if (a.trace && yk == y - 1 && xk == xlo) a.trace[(size_t)task * 8 + 1] = gtime_ns();
-                    if (a.trace && yk == y - 1 && xk == xhi) a.trace[(size_t)task * 8 + 2] = gtime_ns();
-#endif
-                    const int64_t gi = ((int64_t)yk * K + xk) * S + c;
-                    const int sh = (int)(gi & 1);
-                    const unsigned bytes = (unsigned)((ncopy + sh + 1) & ~1) * 8;
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    mbar_expect(full0 + 8 * slot, bytes);
-                    bulk_g2s(ring0 + slot * (unsigned)a.rs * 8, a.lu + (gi - sh), bytes, full0 + 8 * slot);
-                }
-                __syncwarp();
-            };
-            for (int q = 0; q < nk; ++q) {
-                if (warp == 0)
-                    while (qi < nk && qi < q + NR) issue(qi++);
-                const int yk = ylo + q / nx, xk = xlo + q % nx;
-                const unsigned G = kbase + (unsigned)q, slot = G % NR;
-                mbar_wait(full0 + 8 * slot, (G / NR) & 1);
-                const int ox = xk - x, oy = yk - y;
-                if (live && ox >= -r && ox <= r) {
-                    const int s = (ox + r) + W * (oy + r);
-                    if (full_row || ((bits[s >> 5] >> (s & 31)) & 1u)) {
-                        const int64_t k = (int64_t)yk * K + xk;
-                        const int sh = (int)((k * S + c) & 1);
-                        const double *uk = sm + (size_t)NW * bufd + (size_t)slot * a.rs + sh - c;   // uk[c] = pivot
-                        if (lane == 0 && fabs(uk[c]) < a.tol) atomicMin(a.bad, (unsigned long long)(i * g.n + k));
-                        const double l = full_row ? apply_pivot<true, R>(row, colmask, uk, s, ox, oy, r, W, S, c, lane)
-                                                  : apply_pivot<false, R>(row, colmask, uk, s, ox, oy, r, W, S, c, lane);
-                        if (lane == 0) row[s] = l;
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) atomicAdd(&s_cons[slot], 1u);
-            }
-            kbase += (unsigned)nk;
-            if (live)
-                for (int q = lane; q < S; q += 32) __stcg(a.lu + (size_t)i * S + q, row[q]);
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) {
-                __threadfence();
-                *((volatile int *)(a.edone + (size_t)y * a.nb + b)) = 1;
-#ifdef LP_ILU_TRACE
-                if (a.trace) a.trace[(size_t)task * 8 + 3] = gtime_ns();
-#endif
-            }
-            continue;
-        }
-
-        // -------------------------------------------------------- line task L(y)
-        // Rows of the line are taken round-robin by the warps, each row double-
-        // buffered in shared memory.  A row arrives from its block task with all
-        // earlier lines applied and is finished with its in-line pivots x-r..x-1,
-        // read from the sibling warps' buffers.  Requires NW >= r + 1.
-#ifdef LP_ILU_TRACE
-        if (tid == 0 && a.trace) a.trace[(size_t)task * 8] = gtime_ns();
-#endif
-        for (int ix = warp; ix < K; ix += NW) {
-            const int buf = (ix / NW) & 1;
-            double *row = sm + (size_t)(warp * 2 + buf) * bufd;
-            uint32_t *bits = reinterpret_cast<uint32_t *>(row + S);
-            const int64_t i = row0 + ix;
-#ifdef LP_ILU_TRACE
-            const bool trow = a.trace && ix == K / 2 && lane == 0;
-            if (trow) a.trace[(size_t)task * 8 + 4] = gtime_ns();
-#endif
-            if (y >= 1 && lane == 0)
-                while (ld_flag(a.edone + (size_t)y * a.nb + ix / NW) == 0) __nanosleep(64);
-            __syncwarp();
-#ifdef LP_ILU_TRACE
-            if (trow) a.trace[(size_t)task * 8 + 5] = gtime_ns();
-#endif
-            uint32_t *colmask = bits + mwS;
-            for (int q = lane; q < S; q += 32) row[q] = __ldcg(a.lu + (size_t)i * S + q);
-            for (int q = lane; q < g.mw; q += 32) bits[q] = a.mask[(size_t)i * g.mw + q];
-            const bool full_row = __ldg(a.full + i) != 0;
-            __syncwarp();
-            build_colmask(bits, colmask, W, lane);
-            __syncwarp();
-            for (int m = r; m >= 1; --m) {   // pivots x-m, ascending columns
-                const int kix = ix - m;
-                if (kix < 0) continue;
-                const int s = (r - m) + W * r;
-                if (!full_row && !((bits[s >> 5] >> (s & 31)) & 1u)) continue;
-                // back off while polling: 15 spinning warps would otherwise flood the
-                // shared-memory pipe the working warps need
-                while (v_done[kix % (2 * NW)] != kix) __nanosleep(32);
-#ifdef LP_ILU_TRACE
-                unsigned long long tw0 = 0;
-                if (trow && m == 1) tw0 = gtime_ns();
-#endif
-                const double *uk = sm + (size_t)((kix % NW) * 2 + ((kix / NW) & 1)) * bufd;
-                if (lane == 0 && fabs(uk[c]) < a.tol) atomicMin(a.bad, (unsigned long long)(i * g.n + (i - m)));
-                const double l = full_row ? apply_pivot<true, R>(row, colmask, uk, s, -m, 0, r, W, S, c, lane)
-                                          : apply_pivot<false, R>(row, colmask, uk, s, -m, 0, r, W, S, c, lane);
-                if (lane == 0) row[s] = l;
-                __syncwarp();
-#ifdef LP_ILU_TRACE
-                if (trow && m == 1) {
-                    a.trace[(size_t)task * 8 + 1] = tw0;               // overwrite row0 slot
-                    a.trace[(size_t)task * 8 + 4] = gtime_ns() - tw0;  // last apply duration
-                }
-#endif
-            }
-            // siblings may use the row as soon as it is final in shared memory;
-            // other CTAs once it is stored and fenced (per-row flag)
-#ifdef LP_ILU_TRACE
-            if (trow) a.trace[(size_t)task * 8 + 6] = gtime_ns();
-#endif
-            if (lane == 0) v_done[ix % (2 * NW)] = ix;
-            for (int q = lane; q < S; q += 32) __stcg(a.lu + (size_t)i * S + q, row[q]);
-            __threadfence();
-            __syncwarp();
             if (lane == 0) {
-                *((volatile int *)(a.rowf + i)) = 1;
-#ifdef LP_ILU_TRACE
-                if (trow) a.trace[(size_t)task * 8 + 7] = gtime_ns();
-#endif
-#ifdef LP_ILU_TRACE
-                if (a.trace && (ix == 0 || ix == K / 2 || ix == K - 1))
-                    a.trace[(size_t)task * 8 + (ix == 0 ? 1 : (ix == K - 1 ? 3 : 2))] = gtime_ns();
-#endif
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                int minprog = 0;
+                int lastblk = -1;
+                for (int q = 0; q < nk; ++q) {
+                    const int lq = q / nx;
+                    const int yk = ylo + lq, xk = xlo + q - lq * nx;
+                    const unsigned G = gbase + (unsigned)q, slot = G % NRING;
+                    const int bq = lq * nbk + xk / RB - bl;
+                    if (bq != lastblk) {
+                        lastblk = bq;
+                        if (!((dmask >> bq) & 1ull)) {
+                            while (ld_acq_gpu(a.done + yk * a.nb + xk / RB) != a.epoch) __nanosleep(64);
+                            asm volatile("fence.proxy.async.global;" ::: "memory");
+                        }
+                    }
+                    if (G >= NRING && minprog < (int)(G - NRING + 1)) {
+                        for (;;) {
+                            int mp = ld_vol_cta(s_prog);
+#pragma unroll
+                            for (int w = 1; w < NWC; ++w) mp = min(mp, ld_vol_cta(s_prog + w));
+                            minprog = mp;
+                            if (minprog >= (int)(G - NRING + 1)) break;
+                            __nanosleep(20);
+                        }
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    }
+                    const int64_t k = (int64_t)yk * K + xk;
+                    const int64_t gi = k * S + C;
+                    const int sh = (int)(gi & 1);
+                    const unsigned bytes = (unsigned)(((S - C + sh) + 1) & ~1) * 8u;
+                    mbar_expect(mbar0 + 8 * slot, bytes + 16u);
+                    bulk_g2s(smem_addr(ring + (size_t)slot * US), a.lu + (gi - sh), bytes, mbar0 + 8 * slot);
+                    bulk_g2s(smem_addr(rdr + 2 * slot), a.rd + 2 * k, 16u, mbar0 + 8 * slot);
+                }
             }
             __syncwarp();
+            // in-line rows x0-R .. x0-1 of the previous block into the line buffer
+            if (x0 > 0) {
+                if (lane == 0)
+                    while (ld_acq_gpu(a.done + y * a.nb + b - 1) != a.epoch) __nanosleep(64);
+                __syncwarp();
+                for (int xk = max(0, x0 - R); xk < x0; ++xk) {
+                    const int ls = xk - (x0 - R);
+                    const int64_t k = (int64_t)y * K + xk;
+                    const double *g = a.lu + k * S + (C - R);
+                    for (int q = lane; q < S - C + R; q += 32) lbuf[ls * LS + q] = __ldcg(g + q);
+                    if (lane == 0) rcl[ls] = __ldcg(a.rd + 2 * k);
+                    __syncwarp();
+                    if (lane == 0) st_rel_cta(s_lready + ls, task);
+                }
+            }
+        } else {
+            // --------------------------------------------------------- consumers
+            const int xa = x0 + 2 * warp;
+            const bool liveA = xa < K, liveB = xa + 1 < K;
+            const int64_t iA = (int64_t)y * K + xa;
+            const bool colA = lane <= 2 * R, colB = lane >= 1 && lane <= 2 * R + 1;
+            double vA[W], vB[W];
+            unsigned cmA = 0, cmB = 0;
+            {
+                const double *pa = a.src + iA * S + lane, *pb = a.src + (iA + 1) * S + (lane - 1);
+                const bool la = liveA && colA, lb = liveB && colB;
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    vA[j] = la ? ld_stream(pa + W * j) : 0.0;
+                    vB[j] = lb ? ld_stream(pb + W * j) : 0.0;
+                }
+                if (la) cmA = a.full[iA] ? (1u << W) - 1u : colbits<W>(a.mask + iA * a.mw, lane);
+                if (lb) cmB = a.full[iA + 1] ? (1u << W) - 1u : colbits<W>(a.mask + (iA + 1) * a.mw, lane - 1);
+            }
+            // ---- E part: pivot lines y-R .. y-1
+            unsigned G = gbase;
+#pragma unroll
+            for (int j0 = 0; j0 < R; ++j0) {
+                const int yk = y - R + j0;
+                if (yk < 0) continue;
+                for (int xk = xlo; xk <= xhi; ++xk, ++G) {
+                    const int Lk = xk - xa + R;
+                    const unsigned cA = __shfl_sync(FULLM, cmA, Lk & 31);
+                    const unsigned cB = __shfl_sync(FULLM, cmB, Lk & 31);
+                    const bool useA = liveA && Lk >= 0 && Lk <= 2 * R && ((cA >> j0) & 1u);
+                    const bool useB = liveB && Lk >= 1 && Lk <= 2 * R + 1 && ((cB >> j0) & 1u);
+                    if (useA || useB) {
+                        const unsigned slot = G % NRING;
+                        mbar_wait(mbar0 + 8 * slot, (G / NRING) & 1u);
+                        const int64_t k = (int64_t)yk * K + xk;
+                        const int sh = (int)((k * S + C) & 1);
+                        apply2<R>(vA, vB, cmA, cmB, useA, useB, j0, Lk, ring + (size_t)slot * US + sh,
+                                  rdr[2 * slot], lane, a, iA, k);
+                    }
+                    if (lane == 0) st_vol_cta(s_prog + warp, (int)(G + 1));
+                }
+            }
+            // ---- in-line part: rows xa-R .. xa-1 (B: xa-R+1 .. xa)
+#pragma unroll 1
+            for (int m = R; m >= 1; --m) {
+                const int xk = xa - m;
+                if (xk < 0) continue;
+                const int Lk = R - m;
+                const unsigned cA = __shfl_sync(FULLM, cmA, Lk);
+                const unsigned cB = __shfl_sync(FULLM, cmB, Lk);
+                const bool useA = liveA && ((cA >> R) & 1u);
+                const bool useB = liveB && m < R && ((cB >> R) & 1u);
+                if (!useA && !useB) continue;
+                const int ls = xk - (x0 - R);
+                while (ld_acq_cta(s_lready + ls) != task) {
+                }
+                apply2<R>(vA, vB, cmA, cmB, useA, useB, R, Lk, lbuf + (size_t)ls * LS + R, rcl[ls], lane,
+                          a, iA, (int64_t)y * K + xk);
+            }
+            double rcA = 0.0;
+            if (liveA) {
+                // row A is final: line buffer (for the sibling warps) first
+                const int ls = xa - x0 + R;
+                if (colA) {
+#pragma unroll
+                    for (int dy = 0; dy <= R; ++dy) lbuf[ls * LS + lane + W * dy] = vA[R + dy];
+                }
+                if (lane == R) {
+                    rcA = __drcp_rn(vA[R]);
+                    rcl[ls] = rcA;
+                }
+                __syncwarp();
+                if (lane == 0) st_rel_cta(s_lready + ls, task);
+            }
+            double rcB = 0.0;
+            if (liveB) {
+                // row B applies row A from registers (same lane = same column)
+                const unsigned cB = __shfl_sync(FULLM, cmB, R);
+                if ((cB >> R) & 1u) {
+                    const double upiv = __shfl_sync(FULLM, vA[R], R);
+                    const double rc = __shfl_sync(FULLM, rcA, R);
+                    const double lB = qdiv(__shfl_sync(FULLM, vB[R], R), upiv, rc);
+                    if (lane == 0 && fabs(upiv) < a.tol)
+                        atomicMin(a.bad, (unsigned long long)((iA + 1) * a.n + iA));
+                    const int dx = lane - R;
+                    const bool inp = lane <= 2 * R;
+#pragma unroll
+                    for (int dy = 0; dy <= R; ++dy) {
+                        const bool ok = inp && (dy > 0 || dx > 0) && ((cmB >> (R + dy)) & 1u);
+                        if (ok) vB[R + dy] = __dsub_rn(vB[R + dy], __dmul_rn(lB, vA[R + dy]));
+                    }
+                    if (lane == R) vB[R] = lB;
+                }
+                const int ls = xa + 1 - x0 + R;
+                if (colB) {
+#pragma unroll
+                    for (int dy = 0; dy <= R; ++dy) lbuf[ls * LS + (lane - 1) + W * dy] = vB[R + dy];
+                }
+                if (lane == R + 1) {
+                    rcB = __drcp_rn(vB[R]);
+                    rcl[ls] = rcB;
+                }
+                __syncwarp();
+                if (lane == 0) st_rel_cta(s_lready + ls, task);
+            }
+            // global rows and reciprocals (published with the block below)
+            if (liveA && colA) {
+                double *pa = a.lu + iA * S + lane;
+#pragma unroll
+                for (int j = 0; j < W; ++j) pa[W * j] = vA[j];
+                if (lane == R) {
+                    a.rd[2 * iA] = rcA;
+                    a.rd[2 * iA + 1] = 0.0;
+                }
+            }
+            if (liveB && colB) {
+                double *pb = a.lu + (iA + 1) * S + (lane - 1);
+#pragma unroll
+                for (int j = 0; j < W; ++j) pb[W * j] = vB[j];
+                if (lane == R + 1) {
+                    a.rd[2 * iA + 2] = rcB;
+                    a.rd[2 * iA + 3] = 0.0;
+                }
+            }
+        }
+        gbase += (unsigned)nk;
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            st_rel_gpu(a.done + yb, a.epoch);
         }
     }
 }
 
 template <int R>
-int launch_tasks(const TaskArgs &a, size_t smem, cudaStream_t st) {
-    LP_CUDA(cudaFuncSetAttribute(box_ilu0_tasks<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev = 0, nsm = 148, occ = 1;
+int launch(const Args &a, cudaStream_t st) {
+    constexpr int W = 2 * R + 1, S = W * W, C = (S - 1) / 2;
+    constexpr int US = ((S - C + 1) + 1) & ~1;
+    constexpr int LS = ((S - C + R) + 1) & ~1;
+    const size_t smem = ((size_t)NRING * US + 2 * NRING + (size_t)(R + RB) * LS + (R + RB)) * sizeof(double);
+    if (smem > 220 * 1024) {
+        set_error("2-D ILU: %zu bytes of shared memory", smem);
+        return LP_ERR_ARG;
+    }
+    LP_CUDA(cudaFuncSetAttribute(ilu2d_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, nsm = 0, occ = 0;
     LP_CUDA(cudaGetDevice(&dev));
     LP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, box_ilu0_tasks<R>, 32 * NW, smem));
-    if (occ < 1) return LP_ERR_ARG;
+    LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ilu2d_kernel<R>, NTHR, smem));
+    if (occ < 1) {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, ilu2d_kernel<R>);
+        set_error("2-D ILU kernel does not fit an SM (%zu + %zu bytes of shared memory, %d registers, "
+                  "%d threads max, %zu local)", smem, fa.sharedSizeBytes, fa.numRegs,
+                  fa.maxThreadsPerBlock, fa.localSizeBytes);
+        return LP_ERR_ARG;
+    }
     int64_t blocks = (int64_t)occ * nsm;
     if (blocks > a.ntask) blocks = a.ntask;
-    box_ilu0_tasks<R><<<(unsigned)blocks, 32 * NW, smem, st>>>(a);
+    ilu2d_kernel<R><<<(unsigned)blocks, NTHR, smem, st>>>(a);
     count_launch();
     LP_CHECK_LAUNCH();
     return LP_OK;
 }
 
+// tasks (y, b) in key order key = b + 2y (ties by y)
+int task_list(BoxLayout &b, int nb, cudaStream_t st) {
+    const int nlines = (int)(b.n / b.K);
+    const int ntask = nlines * nb;
+    if (b.ilu_tasks && b.ilu_ntask == ntask && b.ilu_nb == nb) return LP_OK;
+    std::vector<int> t;
+    t.reserve(ntask);
+    const int nkeys = nb + 2 * (nlines - 1);
+    for (int key = 0; key < nkeys; ++key)
+        for (int y = 0; y < nlines && 2 * y <= key; ++y) {
+            const int bb = key - 2 * y;
+            if (bb < nb) t.push_back(y * nb + bb);
+        }
+    if (b.ilu_tasks) dfree(b.ilu_tasks);
+    b.ilu_tasks = nullptr;
+    int rc;
+    if ((rc = dalloc(&b.ilu_tasks, (size_t)ntask, "ILU task list"))) return rc;
+    LP_CUDA(cudaMemcpyAsync(b.ilu_tasks, t.data(), (size_t)ntask * sizeof(int), cudaMemcpyHostToDevice, st));
+    LP_CUDA(cudaStreamSynchronize(st));
+    b.ilu_ntask = ntask;
+    b.ilu_nb = nb;
+    return LP_OK;
+}
+
 }  // namespace
 
-// Returns LP_OK after launching, or a negative code when the task kernel does
-// not apply (the caller falls back to the other kernels).
-int box_ilu0_2d_tasks(lp_ilu *m, double tol, unsigned long long *key, const unsigned char *full,
-                      int *edone, cudaStream_t st) {
+// Launches the factorisation of a 2-D box (src -> b.lu); returns a negative
+// code when the kernel does not apply (the caller falls back to the other
+// kernels).  `done` holds nlines * ceil(K / 16) ints.
+int box_ilu0_2d_tasks(lp_ilu *m, const double *src, double tol, unsigned long long *key, int *done,
+                      cudaStream_t st) {
     BoxLayout &b = m->box;
     Geom g = geom_of(b);
-    if (g.d != 2 || g.r + 1 > NW || g.r > 15) return LP_ERR_ARG;
-    const int mwS = (g.mw + 1) & ~1;
-    const size_t bufd = (size_t)g.S + mwS / 2 + 16;
-    const int rs = (int)round_up(g.S - g.c + 1, 2);
-    const size_t smem_l = 2 * NW * bufd * sizeof(double);
-    const size_t smem_e = (NW * bufd + (size_t)NR * rs) * sizeof(double);
-    const size_t smem = smem_l > smem_e ? smem_l : smem_e;
-    if (smem > 220 * 1024) return LP_ERR_ARG;
-    TaskArgs a;
-    a.g = g;
+    if (g.d != 2 || g.r < 1 || g.r > RB || !b.full) return LP_ERR_ARG;
+    const int nb = (int)ceil_div(g.K, RB);
+    int rc;
+    if ((rc = task_list(b, nb, st))) return rc;
+    if (!b.rdiag && (rc = dalloc(&b.rdiag, (size_t)b.n * 2, "ILU reciprocals"))) return rc;
+    Args a;
+    a.K = g.K;
+    a.nlines = g.nlines;
+    a.nb = nb;
+    a.ntask = b.ilu_ntask;
+    a.epoch = 1;
+    a.mw = g.mw;
+    a.n = g.n;
+    a.src = src;
     a.lu = b.lu;
+    a.rd = b.rdiag;
     a.mask = b.mask;
-    a.full = full;
-    a.nb = (g.K + NW - 1) / NW;
-    a.rowf = m->flags;
-    a.edone = edone;
+    a.full = b.full;
+    a.tasks = b.ilu_tasks;
+    a.done = done;
     a.ticket = m->ticket;
     a.tol = tol;
     a.bad = key;
-    a.rs = rs;
-    a.ntask = 1 + (g.nlines - 1) * (a.nb + 1);
-    a.trace = nullptr;
-#ifdef LP_ILU_TRACE
-    {
-        static unsigned long long *tr = nullptr;
-        static size_t trn = 0;
-        if (trn < (size_t)a.ntask * 8) {
-            if (tr) dfree(tr);
-            trn = (size_t)a.ntask * 8;
-            dalloc(&tr, trn, "ilu trace");
-        }
-        cudaMemsetAsync(tr, 0, trn * 8, st);
-        a.trace = tr;
-        g_ilu_trace = tr;
-        g_ilu_trace_n = trn;
-    }
-#endif
     switch (g.r) {
-        case 10: return launch_tasks<10>(a, smem, st);
-        case 12: return launch_tasks<12>(a, smem, st);
-        case 14: return launch_tasks<14>(a, smem, st);
-        default: return launch_tasks<0>(a, smem, st);
+        case 1: return launch<1>(a, st);
+        case 2: return launch<2>(a, st);
+        case 3: return launch<3>(a, st);
+        case 4: return launch<4>(a, st);
+        case 5: return launch<5>(a, st);
+        case 6: return launch<6>(a, st);
+        case 7: return launch<7>(a, st);
+        case 8: return launch<8>(a, st);
+        case 9: return launch<9>(a, st);
+        case 10: return launch<10>(a, st);
+        case 11: return launch<11>(a, st);
+        case 12: return launch<12>(a, st);
+        case 13: return launch<13>(a, st);
+        default: return launch<14>(a, st);
     }
 }
 
 }  // namespace lp
-
-extern "C" int lp_debug_ilu_trace(unsigned long long *host, int64_t n) {
-    if (!lp::g_ilu_trace) return -1;
-    const size_t m = (size_t)n < lp::g_ilu_trace_n ? (size_t)n : lp::g_ilu_trace_n;
-    cudaDeviceSynchronize();
-    cudaMemcpy(host, lp::g_ilu_trace, m * 8, cudaMemcpyDeviceToHost);
-    return (int)m;
-}

@@ -199,7 +199,9 @@ def test_ilu0_csr_bitwise(golden, name, N, T):
 
 @pytest.mark.parametrize("name,N,T", [("cfg4", 12, 8), ("cfg5", 12, 3), ("cfg4", 16, 4),
                                       ("cfg5", 20, 2), ("cfg4", 9, 1), ("cfg2", 20, 10),
-                                      ("cfg2", 520, 4)])
+                                      ("cfg2", 520, 4), ("cfg3", 64, 12), ("cfg3", 150, 12),
+                                      ("cfg2", 100, 10), ("cfg2", 37, 0), ("cfg2", 45, 1),
+                                      ("cfg3", 40, 13)])
 def test_box_factors_bitwise_vs_csr(name, N, T):
     """The box-layout factorisation (3-D: row-per-CTA kernel; 2-D: task graph)
     equals, bit for bit, the CSR kernel on the same M -- which reproduces the
