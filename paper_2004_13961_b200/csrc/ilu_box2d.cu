@@ -43,11 +43,17 @@
 #include "smem_tma.cuh"
 
 namespace lp {
+
+unsigned long long *g_ilu2d_trace = nullptr;   // LP_ILU2D_TRACE builds
+size_t g_ilu2d_trace_n = 0;
+
 namespace {
 
 constexpr int NWC = 7;                 // consumer warps, two rows each (8 warps: 255 registers)
 constexpr int RB = 2 * NWC;            // rows per block task
-constexpr int NRING = 16;              // pivot-row ring slots
+constexpr int NRING = 32;              // pivot-row ring slots
+constexpr int NLR = 16;                // line-buffer slots (>= r + 2): row x in slot x mod 16
+constexpr int LB = 8;                  // pivots issued per loader batch (one per lane)
 constexpr int NTHR = 32 * (NWC + 1);   // + the loader warp
 constexpr unsigned FULLM = 0xffffffffu;
 
@@ -65,7 +71,19 @@ struct Args {
     int *ticket;
     double tol;
     unsigned long long *bad;
+    unsigned long long *trace;    // LP_ILU2D_TRACE builds: [ntask][8] globaltimer stamps
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#ifdef LP_ILU2D_TRACE
+#define TSTAMP(task, slot) atomicMax(a.trace + (size_t)(task) * 8 + (slot), gtime())
+#else
+#define TSTAMP(task, slot) ((void)0)
+#endif
 
 __device__ __forceinline__ int ld_acq_gpu(const int *p) {
     int v;
@@ -91,6 +109,10 @@ __device__ __forceinline__ int ld_vol_cta(const int *p) {
 __device__ __forceinline__ void st_vol_cta(int *p, int v) {
     asm volatile("st.volatile.shared::cta.s32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
 }
+// line-buffer tag of row x0 + dx (-r <= dx < 14) of a task: unique across the
+// slot's reuses (a slot is reused only after every reader of its row is done)
+__device__ __forceinline__ int ltag(int task, int dx) { return (task * 32 + dx + 16) & 0x7fffffff; }
+
 __device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
 
 // correctly rounded a / b from y = RN(1/b) (Markstein)
@@ -115,17 +137,23 @@ __device__ __forceinline__ unsigned colbits(const uint32_t *mrow, int tx) {
 // One pivot application to the warp's two rows.  j0 (static): the pivot's
 // line relative to the rows (j0 = oy + r); Lk: lane of the pivot's column;
 // up[0] = u_kk, up[dx + W dy] = its upper entries; rc = RN(1/u_kk).
-template <int R>
+// FULL (both rows have every slot in the pattern): the updates run
+// unpredicated; entries that must not change are multiplied by a zero
+// multiplier or a zero pivot entry (x - 0 = x exactly), so they keep their bits.
+template <int R, bool FULL>
 __device__ __forceinline__ void apply2(double (&vA)[2 * R + 1], double (&vB)[2 * R + 1],
                                        unsigned cmA, unsigned cmB, bool useA, bool useB, int j0,
-                                       int Lk, const double *up, double rc, int lane,
-                                       const Args &a, int64_t iA, int64_t k) {
+                                       int Lk, const double *up, double rc, const double *zeros,
+                                       int lane, const Args &a, int64_t iA, int64_t k) {
     constexpr int W = 2 * R + 1;
     const int dx = lane - Lk;
     const bool inp = dx >= -R && dx <= R;
+    // lanes outside the pivot's window read a zero block instead (no per-entry selects)
+    const double *ub = inp ? up + dx : zeros;
     double u[R + 1];
+    u[0] = dx > 0 ? ub[0] : 0.0;
 #pragma unroll
-    for (int dy = 0; dy <= R; ++dy) u[dy] = (inp && (dy > 0 || dx > 0)) ? up[dx + W * dy] : 0.0;
+    for (int dy = 1; dy <= R; ++dy) u[dy] = ub[W * dy];
     const double upiv = up[0];
     double aA = 0.0, aB = 0.0;
 #pragma unroll
@@ -134,20 +162,33 @@ __device__ __forceinline__ void apply2(double (&vA)[2 * R + 1], double (&vB)[2 *
             aA = __shfl_sync(FULLM, vA[j], Lk & 31);
             aB = __shfl_sync(FULLM, vB[j], Lk & 31);
         }
-    const double lA = qdiv(aA, upiv, rc), lB = qdiv(aB, upiv, rc);
+    double lA = qdiv(aA, upiv, rc), lB = qdiv(aB, upiv, rc);
     if (lane == 0 && fabs(upiv) < a.tol) {
         if (useA) atomicMin(a.bad, (unsigned long long)(iA * a.n + k));
         if (useB) atomicMin(a.bad, (unsigned long long)((iA + 1) * a.n + k));
     }
+    if (FULL) {
+        const double mA = useA ? lA : 0.0, mB = useB ? lB : 0.0;
 #pragma unroll
-    for (int dy = 0; dy <= R; ++dy) {
+        for (int dy = 0; dy <= R; ++dy) {
 #pragma unroll
-        for (int j = 0; j < W; ++j)
-            if (j == j0 + dy) {
-                const bool ok = inp && (dy > 0 || dx > 0);
-                if (useA && ok && ((cmA >> j) & 1u)) vA[j] = __dsub_rn(vA[j], __dmul_rn(lA, u[dy]));
-                if (useB && ok && ((cmB >> j) & 1u)) vB[j] = __dsub_rn(vB[j], __dmul_rn(lB, u[dy]));
-            }
+            for (int j = 0; j < W; ++j)
+                if (j == j0 + dy) {
+                    vA[j] = __dsub_rn(vA[j], __dmul_rn(mA, u[dy]));
+                    vB[j] = __dsub_rn(vB[j], __dmul_rn(mB, u[dy]));
+                }
+        }
+    } else {
+#pragma unroll
+        for (int dy = 0; dy <= R; ++dy) {
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+                if (j == j0 + dy) {
+                    const bool ok = inp && (dy > 0 || dx > 0);
+                    if (useA && ok && ((cmA >> j) & 1u)) vA[j] = __dsub_rn(vA[j], __dmul_rn(lA, u[dy]));
+                    if (useB && ok && ((cmB >> j) & 1u)) vB[j] = __dsub_rn(vB[j], __dmul_rn(lB, u[dy]));
+                }
+        }
     }
     if (lane == Lk) {
 #pragma unroll
@@ -159,17 +200,104 @@ __device__ __forceinline__ void apply2(double (&vA)[2 * R + 1], double (&vB)[2 *
     }
 }
 
+struct Consumer {
+    int task, y, x0, xlo, xhi, xa, lane, warp;
+    bool liveA, liveB;
+    int64_t iA;
+    unsigned gbase, mbar0;
+    const double *ring, *rdr, *lbuf, *rcl, *zeros;
+    const int *lready;
+    int *prog;
+    int nk;
+};
+
+// E part (pivot lines y-R .. y-1 from the ring) and in-line part (rows
+// xa-R .. xa-1 from the line buffer) of a warp's two rows.
+template <int R, bool FULL>
+__device__ __forceinline__ void consume(const Args &a, const Consumer &c, double (&vA)[2 * R + 1],
+                                        double (&vB)[2 * R + 1], unsigned cmA, unsigned cmB) {
+    constexpr int W = 2 * R + 1, S = W * W, C = (S - 1) / 2;
+    constexpr int US = ((S - C + 1) + 1) & ~1;
+    constexpr int LS = ((S - C + R) + 1) & ~1;
+    const int lane = c.lane, xa = c.xa, y = c.y, K = a.K;
+#ifdef LP_ILU2D_TRACE
+    long long wait_cycles = 0;
+#endif
+    const int nx = c.xhi - c.xlo + 1;
+    const int ylo = y > R ? y - R : 0;
+    // this warp's pivots of a line: columns within r of either row
+    const int xs = max(c.xlo, xa - R), xe = min(c.xhi, xa + 1 + R);
+#pragma unroll
+    for (int j0 = 0; j0 < R; ++j0) {
+        const int yk = y - R + j0;
+        if (yk < 0 || !c.liveA) continue;
+        const unsigned Gl = c.gbase + (unsigned)((yk - ylo) * nx - c.xlo);
+        const int64_t kl = (int64_t)yk * K;
+        for (int xk = xs; xk <= xe; ++xk) {
+            const int Lk = xk - xa + R;
+            bool useA = Lk <= 2 * R;
+            bool useB = c.liveB && Lk >= 1;
+            if (!FULL) {
+                const unsigned cA = __shfl_sync(FULLM, cmA, Lk);
+                const unsigned cB = __shfl_sync(FULLM, cmB, Lk);
+                useA = useA && ((cA >> j0) & 1u);
+                useB = useB && ((cB >> j0) & 1u);
+                if (!useA && !useB) continue;
+            }
+            const unsigned G = Gl + (unsigned)xk, slot = G % NRING;
+            if (lane == 0) st_vol_cta(c.prog + c.warp, (int)G);   // pivots < G done
+#ifdef LP_ILU2D_TRACE
+            const long long tw = clock64();
+            mbar_wait(c.mbar0 + 8 * slot, (G / NRING) & 1u);
+            wait_cycles += clock64() - tw;
+#else
+            mbar_wait(c.mbar0 + 8 * slot, (G / NRING) & 1u);
+#endif
+            const int64_t k = kl + xk;
+            apply2<R, FULL>(vA, vB, cmA, cmB, useA, useB, j0, Lk,
+                            c.ring + (size_t)slot * US + (int)((k ^ C) & 1), c.rdr[2 * slot], c.zeros,
+                            lane, a, c.iA, k);
+        }
+    }
+    if (lane == 0) st_vol_cta(c.prog + c.warp, (int)(c.gbase + c.nk));
+    if (lane == 0) TSTAMP(c.task, 3);
+#ifdef LP_ILU2D_TRACE
+    if (lane == 0) atomicAdd(a.trace + (size_t)c.task * 8 + 6, (unsigned long long)wait_cycles);
+#endif
+#pragma unroll 1
+    for (int m = R; m >= 1; --m) {
+        const int xk = xa - m;
+        if (xk < 0) continue;
+        const int Lk = R - m;
+        bool useA = c.liveA, useB = c.liveB && m < R;
+        if (!FULL) {
+            const unsigned cA = __shfl_sync(FULLM, cmA, Lk);
+            const unsigned cB = __shfl_sync(FULLM, cmB, Lk);
+            useA = useA && ((cA >> R) & 1u);
+            useB = useB && ((cB >> R) & 1u);
+        }
+        if (!useA && !useB) continue;
+        const int ls = xk % NLR;
+        while (ld_acq_cta(c.lready + ls) != ltag(c.task, xk - c.x0)) {
+        }
+        apply2<R, FULL>(vA, vB, cmA, cmB, useA, useB, R, Lk, c.lbuf + (size_t)ls * LS + R, c.rcl[ls],
+                        c.zeros, lane, a, c.iA, (int64_t)y * K + xk);
+    }
+}
+
 template <int R>
 __global__ void __launch_bounds__(NTHR, 1) ilu2d_kernel(const __grid_constant__ Args a) {
     constexpr int W = 2 * R + 1, S = W * W, C = (S - 1) / 2;
     constexpr int US = ((S - C + 1) + 1) & ~1;   // ring slot: diag + upper half (+ alignment)
     constexpr int LS = ((S - C + R) + 1) & ~1;   // line-buffer slot: from slot C - R
-    constexpr int NL = R + RB;                   // line-buffer rows x0 - R .. x0 + RB - 1
+    constexpr int NL = NLR;                      // line-buffer slots (row x -> x mod NLR)
     extern __shared__ __align__(128) double sm[];
     double *ring = sm;                           // [NRING][US]
     double *rdr = ring + NRING * US;             // [NRING][2]
     double *lbuf = rdr + 2 * NRING;              // [NL][LS]
     double *rcl = lbuf + NL * LS;                // [NL]
+    double *zeros = rcl + NL;                    // [W R + 1] zeros
+    for (int i = threadIdx.x; i < W * R + 1; i += NTHR) zeros[i] = 0.0;
     __shared__ __align__(8) unsigned long long mbar[NRING];
     __shared__ int s_lready[NL];
     __shared__ int s_prog[NWC];
@@ -181,7 +309,7 @@ __global__ void __launch_bounds__(NTHR, 1) ilu2d_kernel(const __grid_constant__ 
         for (int i = 0; i < NRING; ++i) mbar_init(mbar0 + 8 * i, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int i = tid; i < NL; i += NTHR) s_lready[i] = -1;
+    for (int i = tid; i < NL; i += NTHR) s_lready[i] = -1;   // never a tag
     if (tid < NWC) s_prog[tid] = 0;
     unsigned gbase = 0;   // ring sequence number of the task's first pivot
     for (;;) {
@@ -197,6 +325,7 @@ __global__ void __launch_bounds__(NTHR, 1) ilu2d_kernel(const __grid_constant__ 
         const int xlo = max(0, x0 - R), xhi = min(K - 1, x0 + RB - 1 + R);
         const int nx = xhi - xlo + 1;
         const int nk = (y - ylo) * nx;
+        if (tid == 0) TSTAMP(task, 0);
 
         if (warp == NWC) {
             // ------------------------------------------------------------ loader
@@ -212,42 +341,55 @@ __global__ void __launch_bounds__(NTHR, 1) ilu2d_kernel(const __grid_constant__ 
                 if (q < nchk) ok = ld_acq_gpu(a.done + (ylo + q / nbk) * a.nb + bl + q % nbk) == a.epoch;
                 dmask |= (unsigned long long)__ballot_sync(FULLM, ok) << q0;
             }
-            if (lane == 0) {
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                int minprog = 0;
-                int lastblk = -1;
-                for (int q = 0; q < nk; ++q) {
-                    const int lq = q / nx;
-                    const int yk = ylo + lq, xk = xlo + q - lq * nx;
-                    const unsigned G = gbase + (unsigned)q, slot = G % NRING;
-                    const int bq = lq * nbk + xk / RB - bl;
-                    if (bq != lastblk) {
-                        lastblk = bq;
-                        if (!((dmask >> bq) & 1ull)) {
-                            while (ld_acq_gpu(a.done + yk * a.nb + xk / RB) != a.epoch) __nanosleep(64);
-                            asm volatile("fence.proxy.async.global;" ::: "memory");
-                        }
-                    }
-                    if (G >= NRING && minprog < (int)(G - NRING + 1)) {
-                        for (;;) {
-                            int mp = ld_vol_cta(s_prog);
+            // pivots go out in batches of LB, lane j issuing pivot q0 + j
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            int minprog = 0;
+            for (int q0 = 0; q0 < nk; q0 += LB) {
+                const int nq = min(LB, nk - q0);
+                const unsigned Glast = gbase + (unsigned)(q0 + nq - 1);
+                if (Glast >= NRING && minprog < (int)(Glast - NRING + 1)) {
+                    // every consumer is past the pivot that last used the batch's slots
+#ifdef LP_ILU2D_TRACE
+                    const long long tw = clock64();
+#endif
+                    for (;;) {
+                        int mp = lane < NWC ? ld_vol_cta(s_prog + lane) : 0x7fffffff;
 #pragma unroll
-                            for (int w = 1; w < NWC; ++w) mp = min(mp, ld_vol_cta(s_prog + w));
-                            minprog = mp;
-                            if (minprog >= (int)(G - NRING + 1)) break;
-                            __nanosleep(20);
-                        }
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        for (int o = 4; o; o >>= 1) mp = min(mp, __shfl_xor_sync(FULLM, mp, o));
+                        minprog = __shfl_sync(FULLM, mp, 0);
+                        if (minprog >= (int)(Glast - NRING + 1)) break;
+                        __nanosleep(20);
                     }
+#ifdef LP_ILU2D_TRACE
+                    if (lane == 0) atomicAdd(a.trace + (size_t)task * 8 + 7, (unsigned long long)(clock64() - tw));
+#endif
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                }
+                const int q = q0 + lane;
+                const bool act = lane < nq;
+                const int lq = q / nx;
+                const int yk = ylo + lq, xk = xlo + q - lq * nx;
+                const int bq = lq * nbk + xk / RB - bl;
+                bool polled = false;
+                if (act && !((dmask >> bq) & 1ull)) {
+                    while (ld_acq_gpu(a.done + yk * a.nb + xk / RB) != a.epoch) __nanosleep(64);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    polled = true;
+                }
+                const unsigned long long pb = polled ? 1ull << bq : 0ull;
+                dmask |= (unsigned long long)__reduce_or_sync(FULLM, (unsigned)pb) |
+                         ((unsigned long long)__reduce_or_sync(FULLM, (unsigned)(pb >> 32)) << 32);
+                if (act) {
+                    const unsigned G = gbase + (unsigned)q, slot = G % NRING;
                     const int64_t k = (int64_t)yk * K + xk;
-                    const int64_t gi = k * S + C;
-                    const int sh = (int)(gi & 1);
+                    const int sh = (int)((k ^ C) & 1);   // parity of k S + C (S odd)
                     const unsigned bytes = (unsigned)(((S - C + sh) + 1) & ~1) * 8u;
                     mbar_expect(mbar0 + 8 * slot, bytes + 16u);
-                    bulk_g2s(smem_addr(ring + (size_t)slot * US), a.lu + (gi - sh), bytes, mbar0 + 8 * slot);
+                    bulk_g2s(smem_addr(ring + (size_t)slot * US), a.lu + (k * S + C - sh), bytes, mbar0 + 8 * slot);
                     bulk_g2s(smem_addr(rdr + 2 * slot), a.rd + 2 * k, 16u, mbar0 + 8 * slot);
                 }
             }
+            if (lane == 0) TSTAMP(task, 1);
             __syncwarp();
             // in-line rows x0-R .. x0-1 of the previous block into the line buffer
             if (x0 > 0) {
@@ -255,15 +397,16 @@ __global__ void __launch_bounds__(NTHR, 1) ilu2d_kernel(const __grid_constant__ 
                     while (ld_acq_gpu(a.done + y * a.nb + b - 1) != a.epoch) __nanosleep(64);
                 __syncwarp();
                 for (int xk = max(0, x0 - R); xk < x0; ++xk) {
-                    const int ls = xk - (x0 - R);
+                    const int ls = xk % NLR;
                     const int64_t k = (int64_t)y * K + xk;
                     const double *g = a.lu + k * S + (C - R);
                     for (int q = lane; q < S - C + R; q += 32) lbuf[ls * LS + q] = __ldcg(g + q);
                     if (lane == 0) rcl[ls] = __ldcg(a.rd + 2 * k);
                     __syncwarp();
-                    if (lane == 0) st_rel_cta(s_lready + ls, task);
+                    if (lane == 0) st_rel_cta(s_lready + ls, ltag(task, xk - x0));
                 }
             }
+            if (lane == 0) TSTAMP(task, 2);
         } else {
             // --------------------------------------------------------- consumers
             const int xa = x0 + 2 * warp;
@@ -283,50 +426,38 @@ __global__ void __launch_bounds__(NTHR, 1) ilu2d_kernel(const __grid_constant__ 
                 if (la) cmA = a.full[iA] ? (1u << W) - 1u : colbits<W>(a.mask + iA * a.mw, lane);
                 if (lb) cmB = a.full[iA + 1] ? (1u << W) - 1u : colbits<W>(a.mask + (iA + 1) * a.mw, lane - 1);
             }
-            // ---- E part: pivot lines y-R .. y-1
-            unsigned G = gbase;
-#pragma unroll
-            for (int j0 = 0; j0 < R; ++j0) {
-                const int yk = y - R + j0;
-                if (yk < 0) continue;
-                for (int xk = xlo; xk <= xhi; ++xk, ++G) {
-                    const int Lk = xk - xa + R;
-                    const unsigned cA = __shfl_sync(FULLM, cmA, Lk & 31);
-                    const unsigned cB = __shfl_sync(FULLM, cmB, Lk & 31);
-                    const bool useA = liveA && Lk >= 0 && Lk <= 2 * R && ((cA >> j0) & 1u);
-                    const bool useB = liveB && Lk >= 1 && Lk <= 2 * R + 1 && ((cB >> j0) & 1u);
-                    if (useA || useB) {
-                        const unsigned slot = G % NRING;
-                        mbar_wait(mbar0 + 8 * slot, (G / NRING) & 1u);
-                        const int64_t k = (int64_t)yk * K + xk;
-                        const int sh = (int)((k * S + C) & 1);
-                        apply2<R>(vA, vB, cmA, cmB, useA, useB, j0, Lk, ring + (size_t)slot * US + sh,
-                                  rdr[2 * slot], lane, a, iA, k);
-                    }
-                    if (lane == 0) st_vol_cta(s_prog + warp, (int)(G + 1));
-                }
-            }
-            // ---- in-line part: rows xa-R .. xa-1 (B: xa-R+1 .. xa)
-#pragma unroll 1
-            for (int m = R; m >= 1; --m) {
-                const int xk = xa - m;
-                if (xk < 0) continue;
-                const int Lk = R - m;
-                const unsigned cA = __shfl_sync(FULLM, cmA, Lk);
-                const unsigned cB = __shfl_sync(FULLM, cmB, Lk);
-                const bool useA = liveA && ((cA >> R) & 1u);
-                const bool useB = liveB && m < R && ((cB >> R) & 1u);
-                if (!useA && !useB) continue;
-                const int ls = xk - (x0 - R);
-                while (ld_acq_cta(s_lready + ls) != task) {
-                }
-                apply2<R>(vA, vB, cmA, cmB, useA, useB, R, Lk, lbuf + (size_t)ls * LS + R, rcl[ls], lane,
-                          a, iA, (int64_t)y * K + xk);
+            {
+                Consumer cs;
+                cs.task = task;
+                cs.y = y;
+                cs.x0 = x0;
+                cs.xlo = xlo;
+                cs.xhi = xhi;
+                cs.xa = xa;
+                cs.lane = lane;
+                cs.warp = warp;
+                cs.liveA = liveA;
+                cs.liveB = liveB;
+                cs.iA = iA;
+                cs.gbase = gbase;
+                cs.mbar0 = mbar0;
+                cs.ring = ring;
+                cs.rdr = rdr;
+                cs.lbuf = lbuf;
+                cs.rcl = rcl;
+                cs.lready = s_lready;
+                cs.prog = s_prog;
+                cs.zeros = zeros;
+                cs.nk = nk;
+                const bool wfull = __all_sync(FULLM, (!liveA || a.full[iA]) && (!liveB || a.full[iA + 1]));
+                if (wfull) consume<R, true>(a, cs, vA, vB, cmA, cmB);
+                else consume<R, false>(a, cs, vA, vB, cmA, cmB);
+                if (lane == 0) TSTAMP(task, 4);
             }
             double rcA = 0.0;
             if (liveA) {
                 // row A is final: line buffer (for the sibling warps) first
-                const int ls = xa - x0 + R;
+                const int ls = xa % NLR;
                 if (colA) {
 #pragma unroll
                     for (int dy = 0; dy <= R; ++dy) lbuf[ls * LS + lane + W * dy] = vA[R + dy];
@@ -336,7 +467,7 @@ __global__ void __launch_bounds__(NTHR, 1) ilu2d_kernel(const __grid_constant__ 
                     rcl[ls] = rcA;
                 }
                 __syncwarp();
-                if (lane == 0) st_rel_cta(s_lready + ls, task);
+                if (lane == 0) st_rel_cta(s_lready + ls, ltag(task, xa - x0));
             }
             double rcB = 0.0;
             if (liveB) {
@@ -357,7 +488,7 @@ __global__ void __launch_bounds__(NTHR, 1) ilu2d_kernel(const __grid_constant__ 
                     }
                     if (lane == R) vB[R] = lB;
                 }
-                const int ls = xa + 1 - x0 + R;
+                const int ls = (xa + 1) % NLR;
                 if (colB) {
 #pragma unroll
                     for (int dy = 0; dy <= R; ++dy) lbuf[ls * LS + (lane - 1) + W * dy] = vB[R + dy];
@@ -367,7 +498,7 @@ __global__ void __launch_bounds__(NTHR, 1) ilu2d_kernel(const __grid_constant__ 
                     rcl[ls] = rcB;
                 }
                 __syncwarp();
-                if (lane == 0) st_rel_cta(s_lready + ls, task);
+                if (lane == 0) st_rel_cta(s_lready + ls, ltag(task, xa + 1 - x0));
             }
             // global rows and reciprocals (published with the block below)
             if (liveA && colA) {
@@ -394,6 +525,7 @@ __global__ void __launch_bounds__(NTHR, 1) ilu2d_kernel(const __grid_constant__ 
         if (tid == 0) {
             __threadfence();
             st_rel_gpu(a.done + yb, a.epoch);
+            TSTAMP(task, 5);
         }
     }
 }
@@ -403,7 +535,8 @@ int launch(const Args &a, cudaStream_t st) {
     constexpr int W = 2 * R + 1, S = W * W, C = (S - 1) / 2;
     constexpr int US = ((S - C + 1) + 1) & ~1;
     constexpr int LS = ((S - C + R) + 1) & ~1;
-    const size_t smem = ((size_t)NRING * US + 2 * NRING + (size_t)(R + RB) * LS + (R + RB)) * sizeof(double);
+    const size_t smem = ((size_t)NRING * US + 2 * NRING + (size_t)NLR * LS + NLR + W * R + 1) *
+                        sizeof(double);
     if (smem > 220 * 1024) {
         set_error("2-D ILU: %zu bytes of shared memory", smem);
         return LP_ERR_ARG;
@@ -485,6 +618,16 @@ int box_ilu0_2d_tasks(lp_ilu *m, const double *src, double tol, unsigned long lo
     a.ticket = m->ticket;
     a.tol = tol;
     a.bad = key;
+    a.trace = nullptr;
+#ifdef LP_ILU2D_TRACE
+    if (g_ilu2d_trace_n < (size_t)a.ntask * 8) {
+        if (g_ilu2d_trace) dfree(g_ilu2d_trace);
+        g_ilu2d_trace_n = (size_t)a.ntask * 8;
+        if ((rc = dalloc(&g_ilu2d_trace, g_ilu2d_trace_n, "ilu trace"))) return rc;
+    }
+    LP_CUDA(cudaMemsetAsync(g_ilu2d_trace, 0, g_ilu2d_trace_n * 8, st));
+    a.trace = g_ilu2d_trace;
+#endif
     switch (g.r) {
         case 1: return launch<1>(a, st);
         case 2: return launch<2>(a, st);
@@ -504,3 +647,13 @@ int box_ilu0_2d_tasks(lp_ilu *m, const double *src, double tol, unsigned long lo
 }
 
 }  // namespace lp
+
+// LP_ILU2D_TRACE builds: per task [start, loader E issued, loader done, last
+// warp E done, last warp done, published] (globaltimer ns); returns the count.
+extern "C" int lp_debug_ilu2d_trace(unsigned long long *host, int64_t n) {
+    if (!lp::g_ilu2d_trace) return -1;
+    const size_t m = (size_t)n < lp::g_ilu2d_trace_n ? (size_t)n : lp::g_ilu2d_trace_n;
+    cudaDeviceSynchronize();
+    cudaMemcpy(host, lp::g_ilu2d_trace, m * 8, cudaMemcpyDeviceToHost);
+    return (int)m;
+}
