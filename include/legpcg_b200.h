@@ -44,6 +44,8 @@ typedef struct lp_ilu lp_ilu;           /* SparseMatrix M and/or IluFactors     
 
 const char *lp_last_error(void);
 const char *lp_version(void);
+/* Number of this library's kernels launched so far by the process (diagnostics). */
+int64_t lp_kernel_launches(void);
 /* Checks that device `device` is an sm_100 part and makes it current. */
 int lp_init(int device);
 

@@ -40,6 +40,7 @@ class LpReport(ctypes.Structure):
 _SIGS = {
     "lp_last_error": (ctypes.c_char_p, []),
     "lp_version": (ctypes.c_char_p, []),
+    "lp_kernel_launches": (_i64, []),
     "lp_init": (_i32, [_i32]),
     "lp_plan_create": (_i32, [_i32, _vp, _vp, ctypes.POINTER(_vp)]),
     "lp_plan_destroy": (_i32, [_vp]),

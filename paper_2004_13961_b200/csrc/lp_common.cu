@@ -64,7 +64,9 @@ void dfree(void *p) {
 
 extern "C" const char *lp_last_error(void) { return lp::t_error.c_str(); }
 
-extern "C" const char *lp_version(void) { return "legpcg_b200 0.1 (sm_100a, fp64)"; }
+extern "C" const char *lp_version(void) { return "legpcg_b200 0.2 (sm_100a, fp64)"; }
+
+extern "C" int64_t lp_kernel_launches(void) { return lp::g_launches; }
 
 extern "C" int lp_init(int device) {
     int count = 0;

@@ -17,13 +17,35 @@ def is_device(a):
     return isinstance(a, t.Tensor) and a.is_cuda
 
 
+_PINNED = {}
+
+
+def _pinned(n):
+    """Cached page-locked staging buffer of n doubles (host side of the copies)."""
+    t = torch()
+    buf = _PINNED.get(n)
+    if buf is None:
+        if len(_PINNED) > 8:
+            _PINNED.clear()
+        buf = t.empty(n, dtype=t.float64, pin_memory=True)
+        _PINNED[n] = buf
+    return buf
+
+
 def to_device(a):
-    """float64 contiguous CUDA tensor holding `a` (numpy/torch) in memory order."""
+    """float64 contiguous CUDA tensor holding `a` (numpy/torch) in memory order.
+    Large host arrays go through a page-locked staging buffer (one DMA)."""
     t = torch()
     _lib.load()
     if isinstance(a, t.Tensor):
         return a.to(device="cuda", dtype=t.float64).contiguous()
     arr = np.ascontiguousarray(a, dtype=np.float64)
+    if arr.size >= (1 << 16):
+        st = _pinned(arr.size)
+        st.numpy()[:] = arr.reshape(-1)
+        out = st.to("cuda", non_blocking=True).reshape(arr.shape)
+        t.cuda.current_stream().synchronize()   # the staging buffer is reused
+        return out
     return t.from_numpy(arr).to("cuda", non_blocking=False)
 
 
