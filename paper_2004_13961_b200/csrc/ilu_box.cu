@@ -687,7 +687,8 @@ int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st) {
     if (hk != none) *bad_row = (int64_t)(hk % (unsigned long long)b.n);
     else if (fabs(plast) < tol) *bad_row = b.n - 1;
     if (*bad_row >= 0) {
-        set_error("zero pivot at elimination step %lld", (long long)*bad_row);
+        set_error("zero pivot at elimination step %lld (row %lld)", (long long)*bad_row,
+                  hk != none ? (long long)(hk / (unsigned long long)b.n) : (long long)(b.n - 1));
         return LP_ERR_ZERO_PIVOT;
     }
     m->factored = true;

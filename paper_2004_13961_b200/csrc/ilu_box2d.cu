@@ -225,27 +225,26 @@ __device__ __forceinline__ void consume(const Args &a, const Consumer &c, double
 #endif
     const int nx = c.xhi - c.xlo + 1;
     const int ylo = y > R ? y - R : 0;
-    // this warp's pivots of a line: columns within r of either row
-    const int xs = max(c.xlo, xa - R), xe = min(c.xhi, xa + 1 + R);
+    // Every warp waits on every ring entry in order, used or not: a slot's
+    // mbarrier only tells the last two phases apart, so a warp may wait on
+    // entry G only once entry G - NRING (same slot) has completed.
 #pragma unroll
     for (int j0 = 0; j0 < R; ++j0) {
         const int yk = y - R + j0;
-        if (yk < 0 || !c.liveA) continue;
+        if (yk < 0) continue;
         const unsigned Gl = c.gbase + (unsigned)((yk - ylo) * nx - c.xlo);
         const int64_t kl = (int64_t)yk * K;
-        for (int xk = xs; xk <= xe; ++xk) {
+        for (int xk = c.xlo; xk <= c.xhi; ++xk) {
+            const unsigned G = Gl + (unsigned)xk, slot = G % NRING;
             const int Lk = xk - xa + R;
-            bool useA = Lk <= 2 * R;
-            bool useB = c.liveB && Lk >= 1;
+            bool useA = c.liveA && Lk >= 0 && Lk <= 2 * R;
+            bool useB = c.liveB && Lk >= 1 && Lk <= 2 * R + 1;
             if (!FULL) {
-                const unsigned cA = __shfl_sync(FULLM, cmA, Lk);
-                const unsigned cB = __shfl_sync(FULLM, cmB, Lk);
+                const unsigned cA = __shfl_sync(FULLM, cmA, Lk & 31);
+                const unsigned cB = __shfl_sync(FULLM, cmB, Lk & 31);
                 useA = useA && ((cA >> j0) & 1u);
                 useB = useB && ((cB >> j0) & 1u);
-                if (!useA && !useB) continue;
             }
-            const unsigned G = Gl + (unsigned)xk, slot = G % NRING;
-            if (lane == 0) st_vol_cta(c.prog + c.warp, (int)G);   // pivots < G done
 #ifdef LP_ILU2D_TRACE
             const long long tw = clock64();
             mbar_wait(c.mbar0 + 8 * slot, (G / NRING) & 1u);
@@ -253,10 +252,13 @@ __device__ __forceinline__ void consume(const Args &a, const Consumer &c, double
 #else
             mbar_wait(c.mbar0 + 8 * slot, (G / NRING) & 1u);
 #endif
-            const int64_t k = kl + xk;
-            apply2<R, FULL>(vA, vB, cmA, cmB, useA, useB, j0, Lk,
-                            c.ring + (size_t)slot * US + (int)((k ^ C) & 1), c.rdr[2 * slot], c.zeros,
-                            lane, a, c.iA, k);
+            if (useA || useB) {
+                const int64_t k = kl + xk;
+                apply2<R, FULL>(vA, vB, cmA, cmB, useA, useB, j0, Lk,
+                                c.ring + (size_t)slot * US + (int)((k ^ C) & 1), c.rdr[2 * slot],
+                                c.zeros, lane, a, c.iA, k);
+            }
+            if (lane == 0) st_vol_cta(c.prog + c.warp, (int)(G + 1));   // entries <= G done
         }
     }
     if (lane == 0) st_vol_cta(c.prog + c.warp, (int)(c.gbase + c.nk));

@@ -215,6 +215,19 @@ def test_box_factors_bitwise_vs_csr(name, N, T):
     assert sha(fb.U.values) == sha(fc.U.values)
 
 
+@pytest.mark.parametrize("case,n,t1", [("example4a", 40, (4, 3)), ("example2b", 30, 5),
+                                       ("example4a", 70, (5, 3))])
+def test_box_factors_bitwise_sparse_patterns(case, n, t1):
+    """Box factors on patterns with holes (per-axis diffusion, zero reaction:
+    most box slots are out of the pattern) equal the CSR kernel's bit for bit."""
+    from paper_2004_13961_b200 import make_problem
+    m = assemble_M(make_problem(case, n), t1, 0)
+    csr = SparseMatrix(m.n, m.indptr, m.indices, m.values)
+    fb, fc = ilu0(m), ilu0(csr)
+    assert sha(fb.L.values) == sha(fc.L.values)
+    assert sha(fb.U.values) == sha(fc.U.values)
+
+
 def test_sparse_known_answers():
     # reference tests/test_sparse.py:144-160
     d = np.array([[1.0, 0, 0], [0.5, 1.0, 0], [0, 0.5, 1.0]])
