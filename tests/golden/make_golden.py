@@ -7,7 +7,7 @@ fixtures next to this script.  The reference's d >= 2 preconditioner solve is
 forced onto its own ILU(0) branch (pcg.py:92-94), as SURVEY.md section 0.2 prescribes.
 
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
-        python tests/golden/make_golden.py
+        python tests/golden/make_golden.py [group ...]      # default: every group
 """
 
 from __future__ import annotations
@@ -167,11 +167,68 @@ def gen_pcg(out):
         print(key, rep.iterations, rep.final_relative_residual, flush=True)
 
 
+STRIDE = 997   # subsample stride of the full-size vectors (stored with sha + probes)
+
+
+def summarise(out, key, v):
+    """A vector too large to commit: sha, probes, norm and a strided subsample."""
+    v = np.asarray(v, dtype=float).ravel(order="C")
+    out[key + "_sha"] = np.array(sha(v))
+    out[key + "_probe"] = probe(v)
+    out[key + "_sub"] = v[::STRIDE].copy()
+
+
+LARGE_MATVEC = [("cfg3", 2048), ("cfg4", 128), ("cfg5", 512)]
+LARGE_TRANSFORMS = [(2, 257), (2, 513), (2, 2049), (1, 2049), (3, 129)]
+LARGE_PRECOND = [("cfg4", 10, 2), ("cfg5", 9, 1)]
+
+
+def gen_large(out):
+    """North-star sizes: full-size matvecs (cfg 3/4/5, C-order K^d inputs from
+    default_rng(7)), transforms at P >= 257, and 3-D reference M + factors."""
+    for name, N in LARGE_MATVEC:
+        w = wl.CONFIGS[name]()
+        spec = ref_spec(w, N)
+        plan = rtr.TransformPlan(N + 1)
+        u = np.random.default_rng(7).standard_normal((N - 1,) * w.dim)
+        v = rop.apply_system(spec, plan, rop.SpectralCoeffs(u)).data
+        summarise(out, f"lmv_{name}_N{N}", v)
+        print("matvec", name, N, flush=True)
+    for d, P in LARGE_TRANSFORMS:
+        plan = rtr.TransformPlan(P)
+        rng = np.random.default_rng(1000 + P + d)
+        c = rng.standard_normal((P,) * d)
+        f = rng.standard_normal((P,) * d)
+        summarise(out, f"ltr{d}d{P}_bdlt", rtr.tensor_bdlt(plan, c))
+        summarise(out, f"ltr{d}d{P}_fdlt", rtr.tensor_fdlt(plan, f))
+        print("transform", d, P, flush=True)
+    for name, N, T in LARGE_PRECOND:
+        w = wl.CONFIGS[name]()
+        spec = ref_spec(w, N)
+        plan = rtr.TransformPlan(N + 1)
+        m = rpre.assemble_M(spec, T, T, plan)
+        key = f"lpc_{name}_N{N}_T{T}"
+        out[key + "_indptr"] = m.indptr.astype(np.int64)
+        out[key + "_indices"] = m.indices.astype(np.int32)
+        out[key + "_values"] = m.values
+        f = rsp.ilu0(m)
+        out[key + "_L_sha"] = np.array(sha(f.L.values))
+        out[key + "_U_sha"] = np.array(sha(f.U.values))
+        r = np.random.default_rng(11).standard_normal(m.n)
+        out[key + "_r"] = r
+        out[key + "_z"] = rsp.precond_apply(f, r)
+        print("precond", key, m.nnz, flush=True)
+
+
+GROUPS = {"quadrature": gen_quadrature, "transforms": gen_transforms, "matvec": gen_matvec,
+          "precond": gen_precond, "pcg": gen_pcg, "large": gen_large}
+
+
 def main():
-    for group, fn in (("quadrature", gen_quadrature), ("transforms", gen_transforms),
-                      ("matvec", gen_matvec), ("precond", gen_precond), ("pcg", gen_pcg)):
+    groups = sys.argv[1:] or list(GROUPS)
+    for group in groups:
         out = {}
-        fn(out)
+        GROUPS[group](out)
         np.savez_compressed(os.path.join(HERE, f"golden_{group}.npz"), **out)
         print("wrote", group, len(out), "arrays", flush=True)
 

@@ -59,6 +59,32 @@ def test_tensor_transforms(golden, d, P):
     assert relerr(tensor_fdlt(plan, g[k + "_f"]), g[k + "_fdlt"]) < 1e-13
 
 
+def check_summary(g, key, v, tol):
+    """Compare a full-size vector with the reference's committed summary
+    (strided subsample, norm and a random projection; make_golden.summarise)."""
+    v = np.asarray(v, dtype=float).ravel()
+    sub = g[key + "_sub"]
+    assert relerr(v[::997], sub) <= tol, (key, relerr(v[::997], sub))
+    pr = g[key + "_probe"]
+    nv = np.linalg.norm(v)
+    assert abs(nv - np.sqrt(pr[3])) <= tol * np.sqrt(pr[3])
+    proj = float(v @ np.random.default_rng(99).standard_normal(v.size))
+    assert abs(proj - pr[2]) <= tol * nv * np.sqrt(v.size)
+
+
+@pytest.mark.parametrize("d,P", [(2, 257), (2, 513), (2, 2049), (1, 2049), (3, 129)])
+def test_tensor_transforms_large(golden, d, P):
+    """tensor_bdlt / tensor_fdlt at the configs' orders (transforms.py:368-375)
+    against the reference run on the same seeded inputs: <= 1e-13."""
+    g = golden("large")
+    rng = np.random.default_rng(1000 + P + d)
+    c = rng.standard_normal((P,) * d)
+    f = rng.standard_normal((P,) * d)
+    plan = TransformPlan(P)
+    check_summary(g, f"ltr{d}d{P}_bdlt", tensor_bdlt(plan, c), 1e-13)
+    check_summary(g, f"ltr{d}d{P}_fdlt", tensor_fdlt(plan, f), 1e-13)
+
+
 def test_transform_known_answers():
     # reference tests/test_transforms.py:22-31,49-59
     plan = TransformPlan(33)
@@ -109,6 +135,17 @@ def test_matvec_full_size_vs_oracle(name, N):
     ref = orc.apply_system(spec, orc.Plan(N + 1), u)
     out = apply_system(spec, TransformPlan(N + 1), SpectralCoeffs(u)).data
     assert relerr(out, ref) < 1e-12
+
+
+@pytest.mark.parametrize("name,N", [("cfg3", 2048), ("cfg4", 128), ("cfg5", 512)])
+def test_matvec_north_star_sizes(golden, name, N):
+    """apply_system (operator.py:204-210) at the full config sizes, 3-D N=512
+    included, against the reference run on the same input: <= 1e-12."""
+    g = golden("large")
+    w = wl.CONFIGS[name]()
+    u = np.random.default_rng(7).standard_normal((N - 1,) * w.dim)
+    v = apply_system(spec_of(w, N), TransformPlan(N + 1), SpectralCoeffs(u)).data
+    check_summary(g, f"lmv_{name}_N{N}", v, 1e-12)
 
 
 def test_matvec_constant_coefficient_known_answers():
@@ -197,7 +234,23 @@ def test_ilu0_csr_bitwise(golden, name, N, T):
     assert relerr(precond_apply(f, g[k + "_r"]), g[k + "_z"]) < 1e-13
 
 
-@pytest.mark.parametrize("name,N,T", [("cfg4", 12, 8), ("cfg5", 12, 3), ("cfg4", 16, 4),
+@pytest.mark.parametrize("name,N,T", [("cfg4", 10, 2), ("cfg5", 9, 1)])
+def test_ilu0_csr_bitwise_3d(golden, name, N, T):
+    """3-D: the CSR kernel on the reference's own M reproduces its factors bit
+    for bit (sparse.py:116-139); with test_box_factors_bitwise_vs_csr this
+    anchors the 3-D box factors to the reference."""
+    g = golden("large")
+    k = f"lpc_{name}_N{N}_T{T}"
+    n = g[k + "_indptr"].size - 1
+    m = SparseMatrix(n, g[k + "_indptr"], g[k + "_indices"], g[k + "_values"])
+    f = ilu0(m)
+    assert sha(f.L.values) == str(g[k + "_L_sha"])
+    assert sha(f.U.values) == str(g[k + "_U_sha"])
+    assert relerr(precond_apply(f, g[k + "_r"]), g[k + "_z"]) < 1e-13
+
+
+@pytest.mark.parametrize("name,N,T", [("cfg4", 10, 2), ("cfg5", 9, 1), ("cfg4", 12, 8),
+                                      ("cfg5", 12, 3), ("cfg4", 16, 4),
                                       ("cfg5", 20, 2), ("cfg4", 9, 1), ("cfg2", 20, 10),
                                       ("cfg2", 520, 4), ("cfg3", 64, 12), ("cfg3", 150, 12),
                                       ("cfg2", 100, 10), ("cfg2", 37, 0), ("cfg2", 45, 1),
@@ -277,6 +330,25 @@ def test_pcg_golden(golden, name, N, T):
     assert abs(rep.iterations - int(g[k + "_iters"])) <= 1
     assert relerr(x.data, g[k + "_x"]) < 1e-10
     assert rep.residual_history.size == rep.iterations + 1
+
+
+@pytest.mark.parametrize("name,N,iters", [("cfg3", 2048, 14), ("cfg4", 64, None)])
+def test_full_size_solve_certificate(name, N, iters):
+    """Full-size ILU(0)-PCG where the CPU oracle cannot run:
+    converged, iteration count as measured, and the residual certificate of
+    the reference's own test (test_pcg.py:49-55) recomputed with the matvec
+    verified above: ||F - (A+B)x|| <= 1.05 eps ||F||."""
+    w = wl.CONFIGS[name](N=N)
+    spec = spec_of(w, N)
+    plan = TransformPlan(N + 1)
+    F = wl.mass_contract_series(w.fhat)
+    x, rep = pcg_solve(spec, SolverConfig(epsilon=w.rtol, preconditioner=(w.T, w.T)), plan,
+                       SpectralCoeffs(F))
+    assert rep.converged, rep.iterations
+    if iters is not None:
+        assert abs(rep.iterations - iters) <= 1, rep.iterations
+    r = F - apply_system(spec, plan, x).data
+    assert np.linalg.norm(r) <= 1.05 * w.rtol * np.linalg.norm(F)
 
 
 def test_pcg_determinism():

@@ -160,3 +160,29 @@ def test_cfg1_rhs_and_accuracy(golden):
     vals = plan.table @ uh
     err = np.sqrt(np.sum(plan.weights * (vals - wl.manufactured_solution_1d()(plan.nodes)) ** 2))
     assert err < 1e-12
+
+
+@pytest.mark.parametrize("name,N,T", [("cfg4", 10, 2), ("cfg5", 9, 1)])
+def test_ilu_3d_reference_M_bitwise(golden, name, N, T):
+    """3-D: the C port's ILU(0) of the reference's own M is bit-identical to the
+    reference's factors; its sweeps equal the reference's."""
+    g = golden("large")
+    k = f"lpc_{name}_N{N}_T{T}"
+    n = g[k + "_indptr"].size - 1
+    mref = sp.csr_matrix((g[k + "_values"], g[k + "_indices"], g[k + "_indptr"]), shape=(n, n))
+    fac = op.ilu0(mref)
+    assert sha(fac.L[2]) == str(g[k + "_L_sha"])
+    assert sha(fac.U[2]) == str(g[k + "_U_sha"])
+    np.testing.assert_array_equal(op.precond_apply(fac, g[k + "_r"]), g[k + "_z"])
+
+
+@pytest.mark.parametrize("d,P", [(2, 257), (2, 513), (1, 2049)])
+def test_transforms_large(golden, d, P):
+    g = golden("large")
+    rng = np.random.default_rng(1000 + P + d)
+    c = rng.standard_normal((P,) * d)
+    f = rng.standard_normal((P,) * d)
+    plan = op.Plan(P)
+    for key, v in ((f"ltr{d}d{P}_bdlt", op.tensor_bdlt(plan, c)),
+                   (f"ltr{d}d{P}_fdlt", op.tensor_fdlt(plan, f))):
+        assert relerr(np.asarray(v).ravel()[::997], g[key + "_sub"]) < 1e-13
