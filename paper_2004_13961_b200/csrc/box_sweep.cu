@@ -72,19 +72,13 @@ __device__ __forceinline__ double ld_poll(const double *p) {
     return v;
 }
 
-// Shared-memory accesses through 32-bit shared-window addresses (computed once;
-// generic pointers make the compiler re-derive the window base every step).
-
-
-
-
-
-
-// A value the compiler must keep in a register (it cannot rematerialise it from
-// the parameter bank, which it otherwise does every iteration of a loop that
-// contains "memory"-clobbering inline asm).
-
-
+// Published values are stored with st.relaxed.gpu and polled with
+// ld.relaxed.gpu: a morally strong pair (no data race under the PTX memory
+// model), and an aligned 8-byte access is single-copy atomic, so a poller sees
+// either the sentinel or the final value.
+__device__ __forceinline__ void st_pub(double *p, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
 
 __device__ __forceinline__ double ring_sent(int t) {
     return __longlong_as_double((long long)(RING_SENT | (unsigned)t));
@@ -129,11 +123,6 @@ __device__ __forceinline__ unsigned long long gtime() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-
-
-
-
-
 
 
 // One TMA bulk copy (two at the ring wrap) of the w-double rows of steps
@@ -317,10 +306,6 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                 constexpr bool hp = decltype(HP)::value;
                 const double q = qn, e1c = e1n, rd = rdn, spt = spn;
                 double c = cn, av = dn;
-#ifdef LP_EXP_ALONE
-                c = 1.0;
-                av = 0.0;
-#else
                 const unsigned long long sb = bits(ring_sent(t));
 #ifdef LP_SWEEP_TRACE
                 while (bits(c) == sb) { c = lds_v(c0 + doff); ++nspin_c; }
@@ -331,15 +316,11 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                 if (hp)
                     while (bits(av) == sb) av = lds_v(d0 + doff);
 #endif
-#endif
                 const double y = fma(-e1, yprev, fma(rd, hp ? c - av : c, -spt));
                 // every lane stores the same values (no divergent branch)
                 sts_v(c0 + doff, ring_sent(t + RING));
                 if (hp) sts_v(d0 + doff, ring_sent(t + RING));
-#ifdef LP_EXP_NOSTORE
-                if (t == Kr - 1)
-#endif
-                __stcg(outp, canon(y));
+                st_pub(outp, canon(y));
                 if (push) st_cluster_f64(push_base + 8u * (unsigned)(FWD ? t : Kr - 1 - t), canon(y));
                 outp += ostep;
                 doff = (doff + 8) & (RING * 8 - 1);
@@ -400,9 +381,6 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
 #endif
             chunk_base += nch;
         } else if (warp == GROUP) {
-#ifdef LP_EXP_ALONE
-            continue;
-#endif
             // ------------------- line L-/+1 group: A_t (the serial forms c_t - A_t)
             // Lane k owns the rows t == k (mod 32) and accumulates their 2r+1
             // products with line L-/+1 as its values arrive (no shuffles on the
@@ -595,16 +573,9 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
             // issue slots
             continue;
         } else {
-#ifdef LP_EXP_ALONE
-            continue;
-#endif
             constexpr int NP = NW / 2;   // warps 0, 1, 4, 5, ... (SMSPs 0 and 1)
             const int pw = (warp >> 2) * 2 + (warp & 1);
-#ifdef LP_EXP_OLDPROD
-            if (false) {
-#else
             if (g.d == 2) {
-#endif
                 // ---- staged producers (2-D).  Stage s = PR consecutive rows (steps
                 // [PR s, PR s + PR)), taken by warp s mod NP.  Their factor rows arrive
                 // by TMA bulk copies into a NSTAGE-slot ring (full/empty mbarriers);
@@ -630,20 +601,6 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                     // slot free: stage gs - NSTAGE (the previous user) consumed
                     while (v_cons[slot] < gs / NSTAGE) {
                     }
-#ifdef LP_EXP_NOPROD
-                    if (true) {
-                        if (lane < nr) {
-                            const int ix = FWD ? t0 + lane : K - 1 - t0 - lane;
-                            const double rv = a.rhs[row0 + ix];
-                            const int tl1 = t1 - 1;
-                            while (bits(v_c[tl1 & (RING - 1)]) != bits(ring_sent(tl1))) __nanosleep(LP_SWEEP_SLEEP);
-                            v_c[(t0 + lane) & (RING - 1)] = rv;
-                        }
-                        __syncwarp();
-                        if (lane == 0) v_cons[slot] = gs / NSTAGE + 1;
-                        continue;
-                    }
-#endif
                     // factor rows: one 16-byte aligned bulk copy per row
                     if (lane == 0) {
                         unsigned bytes = 0;
@@ -769,11 +726,7 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
 #pragma unroll
                 for (int j = 0; j < CH; ++j) {
                     const int jj = b0 + lane + 32 * j;
-#ifdef LP_EXP_NOPROD
-                    dst[j] = 0.0 * jj;
-#else
                     dst[j] = (t < K && jj < a.nslot) ? __ldcs(row + jj) : 0.0;
-#endif
                 }
             };
             auto process = [&](int t, double (&v)[CH], double rhs_i) {
@@ -789,11 +742,7 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                 }
                 __syncwarp();
                 double acc = 0.0;
-#ifdef LP_EXP_NOPROD
-                for (int b0 = 0; b0 < 0; b0 += 32 * CH) {
-#else
                 for (int b0 = 0; b0 < a.nslot; b0 += 32 * CH) {
-#endif
                     if (b0 > 0) {
                         double dummy;
                         load_v(t, v, dummy, b0);
@@ -911,7 +860,7 @@ __global__ void fill_sentinel(int64_t n, double *a, double *b) {
 
 int prefill(int64_t n, double *a, double *b, cudaStream_t st) {
     int64_t blocks = ceil_div(n, 256);
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > num_sms() * 16) blocks = num_sms() * 16;
     fill_sentinel<<<(unsigned)blocks, 256, 0, st>>>(n, a, b);
     count_launch();
     LP_CHECK_LAUNCH();
@@ -929,41 +878,18 @@ int band_stride(const Geom &g) { return band_nq(g) + band_gsz(g); }
 template <bool FWD, int CH, int NQ>
 int run_sweep(SweepArgs a, const Geom &g, size_t smem, cudaStream_t st) {
     constexpr int NW = 16;
-    static int nblocks = 0, csize = 1;
-    static size_t smem_set = 0;
     auto kern = box_sweep_kernel<FWD, NW, CH, NQ>;
-    if (smem_set != smem) {
-        LP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        LP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        int occ = 1, dev = 0, nsm = 148;
-        LP_CUDA(cudaGetDevice(&dev));
-        LP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * NW, smem));
-        nblocks = occ * nsm;
-        csize = 1;
-        // clusters of LP_SWEEP_CLUSTER CTAs when every CTA can be resident
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = LP_SWEEP_CLUSTER;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(LP_SWEEP_CLUSTER, 1, 1);
-        cfg.blockDim = dim3(32 * NW, 1, 1);
-        cfg.dynamicSmemBytes = smem;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        int ncl = 0;
-        if (LP_SWEEP_CLUSTER > 1 && g.K <= 2048 &&
-            cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) == cudaSuccess && ncl > 0) {
-            csize = LP_SWEEP_CLUSTER;
-            nblocks = ncl * LP_SWEEP_CLUSTER;
-        }
-        cudaGetLastError();
-        smem_set = smem;
+    const void *fn = reinterpret_cast<const void *>(kern);
+    // clusters of LP_SWEEP_CLUSTER CTAs (line hand-off through distributed shared
+    // memory) when the hand-off buffer exists (K <= 2048) and every CTA can be resident
+    int csize = 1, blocks = 0;
+    if (LP_SWEEP_CLUSTER > 1 && g.K <= 2048) {
+        blocks = resident_cluster_blocks(fn, 32 * NW, smem, LP_SWEEP_CLUSTER);
+        if (blocks > 0) csize = LP_SWEEP_CLUSTER;
     }
+    if (csize == 1) blocks = resident_blocks(fn, 32 * NW, smem);
+    LP_ARG(blocks > 0, "sweep kernel does not fit an SM (%zu bytes of shared memory)", smem);
     a.csize = csize;
-    int blocks = nblocks;
     if (csize == 1 && blocks > g.nlines) blocks = g.nlines;
     if (csize > 1) {
         const int need = (g.nlines + csize - 1) / csize * csize;
@@ -997,12 +923,11 @@ int launch_nq(const SweepArgs &a, const Geom &g, size_t smem, cudaStream_t st) {
 }
 
 template <bool FWD>
-int launch_sweep(lp_ilu *m, const double *rhs, double *out, cudaStream_t st) {
+int launch_sweep(lp_ilu *m, const double *rhs, double *out, int *ticket, cudaStream_t st) {
     Geom g = geom_of(m->box);
     if (box_sweep3d_applies(g)) {
-        int *tk = m->ticket + (FWD ? 0 : 1);
-        LP_CUDA(cudaMemsetAsync(tk, 0, sizeof(int), st));
-        return box_sweep3d(m, FWD, rhs, out, tk, st);
+        LP_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
+        return box_sweep3d(m, FWD, rhs, out, ticket, st);
     }
     LP_ARG(g.r <= 15, "stencil reach %d > 15 is not supported by the sweep kernel", g.r);
     SweepArgs a;
@@ -1011,7 +936,7 @@ int launch_sweep(lp_ilu *m, const double *rhs, double *out, cudaStream_t st) {
     a.band = FWD ? m->box.band_lo : m->box.band_up;
     a.rhs = rhs;
     a.out = out;
-    a.ticket = m->ticket + (FWD ? 0 : 1);
+    a.ticket = ticket;
     const int nq = band_nq(g);
     a.gsz = band_gsz(g);
     a.band_g = a.band + (size_t)g.n * nq;
@@ -1066,27 +991,27 @@ int box_build_bands(lp_ilu *m, cudaStream_t st) {
                        (rc = dalloc(&b.band_up, (size_t)b.n * bs, "band")) ||
                        (rc = dalloc(&b.diag, (size_t)b.n, "diag"))))
         return rc;
-    band_kernel<<<148 * 8, 256, 0, st>>>(g, b.lu, band_nq(g), band_gsz(g), b.band_lo, b.band_up, b.diag);
+    band_kernel<<<num_sms() * 8, 256, 0, st>>>(g, b.lu, band_nq(g), band_gsz(g), b.band_lo, b.band_up, b.diag);
     count_launch();
     LP_CHECK_LAUNCH();
     return LP_OK;
 }
 
-int box_forward(lp_ilu *m, const double *r, double *y, cudaStream_t st) {
+int box_forward(lp_ilu *m, const double *r, double *y, int *ticket, cudaStream_t st) {
     int rc = prefill(m->n, y, nullptr, st);
-    return rc ? rc : launch_sweep<true>(m, r, y, st);
+    return rc ? rc : launch_sweep<true>(m, r, y, ticket, st);
 }
 
-int box_backward(lp_ilu *m, const double *y, double *z, cudaStream_t st) {
+int box_backward(lp_ilu *m, const double *y, double *z, int *ticket, cudaStream_t st) {
     int rc = prefill(m->n, z, nullptr, st);
-    return rc ? rc : launch_sweep<false>(m, y, z, st);
+    return rc ? rc : launch_sweep<false>(m, y, z, ticket, st);
 }
 
 // precond_apply: one prefill of both outputs, then the two sweeps.
-int box_apply(lp_ilu *m, const double *r, double *z, cudaStream_t st) {
-    int rc = prefill(m->n, m->ytmp, z, st);
-    if (!rc) rc = launch_sweep<true>(m, r, m->ytmp, st);
-    if (!rc) rc = launch_sweep<false>(m, m->ytmp, z, st);
+int box_apply(lp_ilu *m, const double *r, double *z, const SweepScratch &s, cudaStream_t st) {
+    int rc = prefill(m->n, s.ytmp, z, st);
+    if (!rc) rc = launch_sweep<true>(m, r, s.ytmp, s.tickets, st);
+    if (!rc) rc = launch_sweep<false>(m, s.ytmp, z, s.tickets + 1, st);
     return rc;
 }
 

@@ -115,7 +115,7 @@ __device__ __forceinline__ double ld_l2(const double *p, unsigned long long pol)
 // through it (evict_first): a consumer's poll must not queue behind the
 // stream's HBM traffic.
 __device__ __forceinline__ void st_keep(double *p, double v, unsigned long long pol) {
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+    asm volatile("st.relaxed.gpu.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
 __device__ __forceinline__ bool is_sent(double v) {
@@ -623,21 +623,11 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
 template <bool FWD, int R>
 int launch3m(const Sweep3Args &a, cudaStream_t st) {
     using G = S3m<R>;
-    static int nblocks = 0;
-    static size_t smem_set = 0;
     const size_t smem = ((size_t)G::NR * G::LPB * G::ROWD + (size_t)G::LPB * a.g.K) * sizeof(double);
     LP_ARG(smem <= 227 * 1024, "3-D sweep needs %zu bytes of shared memory (K = %d)", smem, a.g.K);
     auto kern = box_sweep3d_multi_kernel<FWD, R>;
-    if (smem > smem_set) {
-        LP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int occ = 1, dev = 0, nsm = 148;
-        LP_CUDA(cudaGetDevice(&dev));
-        LP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::NT, smem));
-        if (occ < 1) return LP_ERR_ARG;
-        nblocks = occ * nsm;
-        smem_set = smem;
-    }
+    const int nblocks = resident_blocks(reinterpret_cast<const void *>(kern), G::NT, smem);
+    if (nblocks < 1) return LP_ERR_ARG;
     int blocks = nblocks < a.ngroups ? nblocks : a.ngroups;
     kern<<<blocks, G::NT, smem, st>>>(a);
     count_launch();
@@ -648,21 +638,11 @@ int launch3m(const Sweep3Args &a, cudaStream_t st) {
 template <bool FWD, int R>
 int launch3(const Sweep3Args &a, cudaStream_t st) {
     using G = S3<R>;
-    static int nblocks = 0;
-    static size_t smem_set = 0;
     const size_t smem = ((size_t)G::NR * G::ROWD + a.g.K) * sizeof(double);
     LP_ARG(smem <= 227 * 1024, "3-D sweep needs %zu bytes of shared memory (K = %d)", smem, a.g.K);
     auto kern = box_sweep3d_kernel<FWD, R>;
-    if (smem > smem_set) {   // the rhs staging grows with the line length K
-        LP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int occ = 1, dev = 0, nsm = 148;
-        LP_CUDA(cudaGetDevice(&dev));
-        LP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::NT, smem));
-        if (occ < 1) return LP_ERR_ARG;
-        nblocks = occ * nsm;
-        smem_set = smem;
-    }
+    const int nblocks = resident_blocks(reinterpret_cast<const void *>(kern), G::NT, smem);
+    if (nblocks < 1) return LP_ERR_ARG;
     int blocks = nblocks < a.g.nlines ? nblocks : a.g.nlines;
     kern<<<blocks, G::NT, smem, st>>>(a);
     count_launch();
@@ -755,7 +735,8 @@ static int small_reach_lpb(int r) {
 }
 
 // The caller has pre-filled `out` with the sentinel and reset the ticket.
-int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket, cudaStream_t st) {
+int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket, cudaStream_t st,
+                const RankLayout *ranks) {
     Geom g = geom_of(m->box);
     if (!box_sweep3d_applies(g)) return LP_ERR_ARG;
     int rc = ensure_line_order(m->box, st);
@@ -776,11 +757,11 @@ int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket
     a.ys[1] = g.K;
     a.rep_stride = 0;
     a.rhs_stride = 0;
-    if (m->sweep_nranks > 1) {
-        a.nranks = m->sweep_nranks;
-        for (int v = 0; v <= a.nranks; ++v) a.ys[v] = m->sweep_ys[v];
+    if (ranks && ranks->nranks > 1) {
+        a.nranks = ranks->nranks;
+        for (int v = 0; v <= a.nranks; ++v) a.ys[v] = ranks->ys[v];
         a.rep_stride = g.n;
-        a.rhs_stride = m->sweep_rhs_replicated ? g.n : 0;
+        a.rhs_stride = ranks->rhs_replicated ? g.n : 0;
     }
     a.trace = nullptr;
 #ifdef LP_SWEEP_TRACE
@@ -829,16 +810,18 @@ extern "C" int lp_sweep_ranks(lp_ilu *f, int nranks, const int *ys, int dir, con
     LP_ARG(ys[0] == 0 && ys[nranks] == g.K, "y slabs must cover [0, K)");
     for (int v = 0; v < nranks; ++v) LP_ARG(ys[v] < ys[v + 1], "empty y slab");
     cudaStream_t st = as_stream(stream);
-    fill_sent3<<<148 * 8, 256, 0, st>>>((int64_t)nranks * g.n, out);
+    fill_sent3<<<num_sms() * 8, 256, 0, st>>>((int64_t)nranks * g.n, out);
     count_launch();
-    int *tk = f->ticket + (dir == 0 ? 0 : 1);
+    RankLayout lay;
+    lay.nranks = nranks;
+    for (int v = 0; v <= nranks; ++v) lay.ys[v] = ys[v];
+    lay.rhs_replicated = rhs_replicated != 0;
+    int *tk = nullptr;
+    int rc;
+    if ((rc = salloc(&tk, 1, "sweep ticket", st))) return rc;
     LP_CUDA(cudaMemsetAsync(tk, 0, sizeof(int), st));
-    f->sweep_nranks = nranks;
-    for (int v = 0; v <= nranks; ++v) f->sweep_ys[v] = ys[v];
-    f->sweep_rhs_replicated = rhs_replicated != 0;
-    const int rc = box_sweep3d(f, dir == 0, rhs, out, tk, st);
-    f->sweep_nranks = 1;
-    f->sweep_rhs_replicated = false;
+    rc = box_sweep3d(f, dir == 0, rhs, out, tk, st, &lay);
+    sfree(tk, st);
     return rc;
 }
 

@@ -54,28 +54,42 @@ struct lp_ilu {
     int epoch = 0;
     int *ticket = nullptr;      // dynamic row tickets (2 counters)
     int64_t *bad = nullptr;     // zero-pivot key (device)
-    double *ytmp = nullptr;     // forward-sweep result for precond_apply
     int64_t missing_diag = -1;  // first row without a stored diagonal (box assembly)
-    // 3-D sweeps over y-slab ranks emulated on one device (lp_sweep_ranks)
-    int sweep_nranks = 1;
-    int sweep_ys[9] = {0};
-    bool sweep_rhs_replicated = false;
 };
 
 namespace lp {
-int ilu_apply(lp_ilu *m, const double *r, double *z, cudaStream_t st);
-int box_forward(lp_ilu *m, const double *r, double *y, cudaStream_t st);
-int box_backward(lp_ilu *m, const double *y, double *z, cudaStream_t st);
+// Per-call sweep state (stream-ordered scratch): the sweeps never write to the
+// handle, so concurrent precond_apply / pcg_solve calls on one set of factors
+// (different streams or threads) are independent.
+struct SweepScratch {
+    double *ytmp = nullptr;   // [n] forward-sweep result of precond_apply
+    int *tickets = nullptr;   // [2] line / row tickets (forward, backward)
+    int *flags = nullptr;     // [n] CSR sweeps: per-row progress
+};
+int scratch_alloc(const lp_ilu *m, SweepScratch &s, cudaStream_t st);
+void scratch_free(SweepScratch &s, cudaStream_t st);
+// 3-D sweeps with the vector distributed over y-slab ranks (lp_sweep_ranks)
+struct RankLayout {
+    int nranks = 1;
+    int ys[9] = {0};
+    bool rhs_replicated = false;
+};
+int ilu_apply(lp_ilu *m, const double *r, double *z, const SweepScratch &s, cudaStream_t st);
+int ilu_forward(lp_ilu *m, const double *r, double *y, const SweepScratch &s, cudaStream_t st);
+int ilu_backward(lp_ilu *m, const double *y, double *z, const SweepScratch &s, cudaStream_t st);
+int box_forward(lp_ilu *m, const double *r, double *y, int *ticket, cudaStream_t st);
+int box_backward(lp_ilu *m, const double *y, double *z, int *ticket, cudaStream_t st);
 int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st);
 int box_spmv(lp_ilu *m, const double *x, double *y, cudaStream_t st);
 int box_export(const lp_ilu *m, int which, int64_t *indptr, int32_t *indices, double *values);
 int box_build_bands(lp_ilu *m, cudaStream_t st);
-int box_apply(lp_ilu *m, const double *r, double *z, cudaStream_t st);
+int box_apply(lp_ilu *m, const double *r, double *z, const SweepScratch &s, cudaStream_t st);
 int box_ilu0_2d_tasks(lp_ilu *m, const double *src, double tol, unsigned long long *key, int *done,
                       cudaStream_t st);
 int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_t st);
 struct Geom;
 bool box_sweep3d_applies(const Geom &g);
 int ensure_line_order(BoxLayout &b, cudaStream_t st);
-int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket, cudaStream_t st);
+int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket, cudaStream_t st,
+                const RankLayout *ranks = nullptr);
 }  // namespace lp

@@ -612,7 +612,7 @@ int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st) {
                         (size_t)g.mw * sizeof(uint32_t) + 16;
     int dev;
     LP_CUDA(cudaGetDevice(&dev));
-    int nsm = 148;
+    int nsm = 0;
     LP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     constexpr int LNW = 16;
     const size_t line_smem = (size_t)2 * LNW * (g.S + ((g.mw + 1) & ~1) / 2) * sizeof(double);
@@ -793,8 +793,7 @@ extern "C" int lp_box_assemble(int d, int K, int n_groups, const int *lens, cons
         (rc = dalloc(&dhats, hat_total, "hats")) || (rc = dalloc(&dblocks, nblk, "1-D blocks")) ||
         (rc = dalloc(&cnt, 2, "counters")) ||
         (rc = dalloc(&m->flags, b.n > 2 * (b.n / K) + 2 ? b.n : 2 * (b.n / K) + 2, "flags")) ||
-        (rc = dalloc(&m->ticket, 4, "tickets")) || (rc = dalloc(&m->bad, 1, "pivot key")) ||
-        (rc = dalloc(&m->ytmp, b.n, "sweep vector")))
+        (rc = dalloc(&m->ticket, 4, "tickets")) || (rc = dalloc(&m->bad, 1, "pivot key")))
         return fail(rc);
     for (int gi = 0; gi < n_groups; ++gi) {
         const GroupDesc &G = a.grp[gi];
@@ -825,9 +824,9 @@ extern "C" int lp_box_assemble(int d, int K, int n_groups, const int *lens, cons
     } else {
         // general reach / degree: raw products, symmetrisation, pattern (three passes)
         box_raw_kernel<<<dim3((unsigned)a.g.nlines, slot_lines), 128>>>(a, b.values);
-        box_sym_kernel<<<148 * 8, 256>>>(a.g, b.values);
-        box_mask_kernel<<<148 * 8, 256>>>(a.g, b.values, b.mask, cnt, cnt + 1);
-        box_full_kernel<<<148 * 8, 256>>>(a.g, b.mask, b.full);
+        box_sym_kernel<<<num_sms() * 8, 256>>>(a.g, b.values);
+        box_mask_kernel<<<num_sms() * 8, 256>>>(a.g, b.values, b.mask, cnt, cnt + 1);
+        box_full_kernel<<<num_sms() * 8, 256>>>(a.g, b.mask, b.full);
         count_launch(4);
     }
     unsigned long long host[2];

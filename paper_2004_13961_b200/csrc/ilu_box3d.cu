@@ -392,7 +392,7 @@ int launch3(const Ilu3Args &a, cudaStream_t st) {
                         (size_t)a.g.mw * sizeof(uint32_t) + (size_t)G::C * sizeof(int) + 16;
     LP_CUDA(cudaFuncSetAttribute(box_ilu0_3d_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    int dev = 0, nsm = 148, occ = 1;
+    int dev = 0, nsm = 0, occ = 1;
     LP_CUDA(cudaGetDevice(&dev));
     LP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, box_ilu0_3d_kernel<R>, G::TPB, smem));

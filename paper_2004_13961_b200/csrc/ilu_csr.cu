@@ -173,25 +173,26 @@ __global__ void spmv_csr_kernel(int64_t n, const int64_t *__restrict__ indptr,
 
 unsigned syncfree_blocks(int64_t n) {
     int64_t b = ceil_div(n, WARPS_PER_BLOCK);
-    const int64_t cap = 148 * 8;
+    const int64_t cap = (int64_t)num_sms() * 8;
     return (unsigned)(b < cap ? b : cap);
 }
 
-int csr_fwd(lp_ilu *m, const double *r, double *y, cudaStream_t st) {
-    const int ep = ++m->epoch;
-    LP_CUDA(cudaMemsetAsync(m->ticket, 0, sizeof(int), st));
+// per-call progress flags (zeroed, epoch 1) and ticket
+int csr_fwd(lp_ilu *m, const double *r, double *y, int *flags, int *ticket, cudaStream_t st) {
+    LP_CUDA(cudaMemsetAsync(flags, 0, m->n * sizeof(int), st));
+    LP_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
     fwd_csr_kernel<<<syncfree_blocks(m->n), 32 * WARPS_PER_BLOCK, 0, st>>>(
-        m->n, m->indptr, m->indices, m->diag, m->lu, r, y, m->flags, ep, m->ticket);
+        m->n, m->indptr, m->indices, m->diag, m->lu, r, y, flags, 1, ticket);
     count_launch();
     LP_CHECK_LAUNCH();
     return LP_OK;
 }
 
-int csr_bwd(lp_ilu *m, const double *y, double *z, cudaStream_t st) {
-    const int ep = ++m->epoch;
-    LP_CUDA(cudaMemsetAsync(m->ticket, 0, sizeof(int), st));
+int csr_bwd(lp_ilu *m, const double *y, double *z, int *flags, int *ticket, cudaStream_t st) {
+    LP_CUDA(cudaMemsetAsync(flags, 0, m->n * sizeof(int), st));
+    LP_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
     bwd_csr_kernel<<<syncfree_blocks(m->n), 32 * WARPS_PER_BLOCK, 0, st>>>(
-        m->n, m->indptr, m->indices, m->diag, m->lu, y, z, m->flags, ep, m->ticket);
+        m->n, m->indptr, m->indices, m->diag, m->lu, y, z, flags, 1, ticket);
     count_launch();
     LP_CHECK_LAUNCH();
     return LP_OK;
@@ -199,11 +200,37 @@ int csr_bwd(lp_ilu *m, const double *y, double *z, cudaStream_t st) {
 
 }  // namespace
 
-int ilu_apply(lp_ilu *m, const double *r, double *z, cudaStream_t st) {
+int scratch_alloc(const lp_ilu *m, SweepScratch &s, cudaStream_t st) {
     int rc;
-    if (m->kind == MAT_BOX) return box_apply(m, r, z, st);
-    if ((rc = csr_fwd(m, r, m->ytmp, st))) return rc;
-    return csr_bwd(m, m->ytmp, z, st);
+    if ((rc = salloc(&s.ytmp, (size_t)m->n, "sweep vector", st)) ||
+        (rc = salloc(&s.tickets, 2, "sweep tickets", st)))
+        return rc;
+    if (m->kind != MAT_BOX && (rc = salloc(&s.flags, (size_t)m->n, "sweep flags", st))) return rc;
+    return LP_OK;
+}
+
+void scratch_free(SweepScratch &s, cudaStream_t st) {
+    sfree(s.ytmp, st);
+    sfree(s.tickets, st);
+    sfree(s.flags, st);
+    s = SweepScratch{};
+}
+
+int ilu_apply(lp_ilu *m, const double *r, double *z, const SweepScratch &s, cudaStream_t st) {
+    int rc;
+    if (m->kind == MAT_BOX) return box_apply(m, r, z, s, st);
+    if ((rc = csr_fwd(m, r, s.ytmp, s.flags, s.tickets, st))) return rc;
+    return csr_bwd(m, s.ytmp, z, s.flags, s.tickets + 1, st);
+}
+
+int ilu_forward(lp_ilu *m, const double *r, double *y, const SweepScratch &s, cudaStream_t st) {
+    if (m->kind == MAT_BOX) return box_forward(m, r, y, s.tickets, st);
+    return csr_fwd(m, r, y, s.flags, s.tickets, st);
+}
+
+int ilu_backward(lp_ilu *m, const double *y, double *z, const SweepScratch &s, cudaStream_t st) {
+    if (m->kind == MAT_BOX) return box_backward(m, y, z, s.tickets + 1, st);
+    return csr_bwd(m, y, z, s.flags, s.tickets + 1, st);
 }
 
 }  // namespace lp
@@ -213,7 +240,7 @@ using namespace lp;
 static int alloc_sweep_state(lp_ilu *m) {
     int rc;
     if ((rc = dalloc(&m->flags, m->n, "row flags")) || (rc = dalloc(&m->ticket, 4, "tickets")) ||
-        (rc = dalloc(&m->bad, 1, "pivot key")) || (rc = dalloc(&m->ytmp, m->n, "sweep vector")))
+        (rc = dalloc(&m->bad, 1, "pivot key")))
         return rc;
     LP_CUDA(cudaMemset(m->flags, 0, m->n * sizeof(int)));
     return LP_OK;
@@ -252,7 +279,7 @@ extern "C" int lp_ilu_destroy(lp_ilu *m) {
     if (!m) return LP_OK;
     cudaDeviceSynchronize();
     void *ptrs[] = {m->indptr, m->indices, m->values, m->lu, m->diag, m->flags, m->ticket,
-                    m->bad, m->ytmp, m->box.values, m->box.lu, m->box.mask,
+                    m->bad, m->box.values, m->box.lu, m->box.mask,
                     m->box.band_lo, m->box.band_up, m->box.diag, m->box.line_order,
                     m->box.line_groups, m->box.full, m->box.ilu_tasks, m->box.rdiag};
     for (void *p : ptrs)
@@ -307,21 +334,33 @@ extern "C" int lp_ilu0(lp_ilu *m, double tol, int64_t *bad_row, void *stream) {
     return LP_OK;
 }
 
+// The sweeps run on per-call stream-ordered scratch (reentrant: concurrent
+// calls on one set of factors from different streams or threads are safe).
+template <class F>
+static int with_scratch(lp_ilu *m, cudaStream_t st, F &&body) {
+    SweepScratch s;
+    int rc = scratch_alloc(m, s, st);
+    if (!rc) rc = body(s);
+    scratch_free(s, st);
+    return rc;
+}
+
 extern "C" int lp_forward_sub(lp_ilu *m, const double *r, double *y, void *stream) {
     LP_ARG(m->factored, "matrix has not been factored (call lp_ilu0)");
-    if (m->kind == MAT_BOX) return box_forward(m, r, y, as_stream(stream));
-    return csr_fwd(m, r, y, as_stream(stream));
+    cudaStream_t st = as_stream(stream);
+    return with_scratch(m, st, [&](const SweepScratch &s) { return ilu_forward(m, r, y, s, st); });
 }
 
 extern "C" int lp_backward_sub(lp_ilu *m, const double *y, double *z, void *stream) {
     LP_ARG(m->factored, "matrix has not been factored (call lp_ilu0)");
-    if (m->kind == MAT_BOX) return box_backward(m, y, z, as_stream(stream));
-    return csr_bwd(m, y, z, as_stream(stream));
+    cudaStream_t st = as_stream(stream);
+    return with_scratch(m, st, [&](const SweepScratch &s) { return ilu_backward(m, y, z, s, st); });
 }
 
 extern "C" int lp_precond_apply(lp_ilu *m, const double *r, double *z, void *stream) {
     LP_ARG(m->factored, "matrix has not been factored (call lp_ilu0)");
-    return ilu_apply(m, r, z, as_stream(stream));
+    cudaStream_t st = as_stream(stream);
+    return with_scratch(m, st, [&](const SweepScratch &s) { return ilu_apply(m, r, z, s, st); });
 }
 
 extern "C" int lp_spmv(lp_ilu *m, const double *x, double *y, void *stream) {

@@ -370,20 +370,16 @@ void lt_set_out(LtArgs &a, int oi, double *out, const double *grid) {
 }
 
 int line_transform(const LtArgs &a, cudaStream_t st) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        LP_CUDA(cudaFuncSetAttribute(line_transform_kernel<1>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)SMEM_BYTES));
-        LP_CUDA(cudaFuncSetAttribute(line_transform_kernel<2>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)SMEM_BYTES));
-        attr_set = true;
+    // per device (cached): sets the kernels' dynamic shared-memory limit
+    if (resident_blocks(reinterpret_cast<const void *>(line_transform_kernel<1>), THREADS, SMEM_BYTES) < 1 ||
+        resident_blocks(reinterpret_cast<const void *>(line_transform_kernel<2>), THREADS, SMEM_BYTES) < 1) {
+        set_error("line transform kernel does not fit an SM");
+        return LP_ERR_CUDA;
     }
     if (a.B <= 0 || a.nouts <= 0) return LP_OK;
     dim3 grid((unsigned)ceil_div(a.B, BN), (unsigned)(a.Mdim / BM), (unsigned)a.nouts);
     const int64_t ctas = (int64_t)grid.x * grid.y * grid.z;
-    if (ctas > 2 * 148)
+    if (ctas > 2 * num_sms())
         line_transform_kernel<2><<<grid, THREADS, SMEM_BYTES, st>>>(a);
     else
         line_transform_kernel<1><<<grid, THREADS, SMEM_BYTES, st>>>(a);

@@ -34,13 +34,34 @@ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 // Device allocation that records an LP_ERR_OOM message on failure.
 int dalloc(void **p, size_t bytes, const char *what);
-// Release a dalloc'd buffer (stream-ordered on the legacy stream; callers that
-// may still have work in flight on other streams synchronise first).
-void dfree(void *p);
+// Release a dalloc'd buffer, stream-ordered after the work already queued on
+// `st` (the legacy stream by default; pass the stream that last used it).
+void dfree(void *p, cudaStream_t st = nullptr);
 template <class T>
 int dalloc(T **p, size_t count, const char *what) {
     return dalloc(reinterpret_cast<void **>(p), count * sizeof(T), what);
 }
+
+// Multiprocessor count of the current device (cached per device).
+int num_sms();
+// Stream-ordered scratch from the device pool: no device synchronisation, so
+// per-call workspaces are cheap and concurrent calls on different streams get
+// their own buffers.  The buffer may be used on `st` only (or after an event).
+int salloc(void **p, size_t bytes, const char *what, cudaStream_t st);
+template <class T>
+int salloc(T **p, size_t count, const char *what, cudaStream_t st) {
+    return salloc(reinterpret_cast<void **>(p), count * sizeof(T), what, st);
+}
+void sfree(void *p, cudaStream_t st);
+
+// Resident CTAs of kernel `fn` on the whole device (occupancy x SMs) with
+// `threads` per CTA and `smem` dynamic shared memory; sets the kernel's
+// dynamic-smem limit first.  Cached per (device, kernel, threads, smem),
+// thread-safe.  Returns 0 when the kernel does not fit an SM.
+int resident_blocks(const void *fn, int threads, size_t smem);
+// Same for thread-block clusters of `csize` CTAs (non-portable sizes allowed):
+// resident clusters x csize, or 0.
+int resident_cluster_blocks(const void *fn, int threads, size_t smem, int csize);
 
 // Count of this library's kernel launches (reported by the PCG loop).
 extern int64_t g_launches;

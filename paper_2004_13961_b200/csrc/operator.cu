@@ -271,9 +271,6 @@ extern "C" int lp_operator_create(lp_plan *plan, int d, const double *beta_grid,
                                                                          plan->weights, op->alpha_w);
         count_launch();
     }
-    if ((rc = dalloc(&op->wsA, 4 * nP, "operator workspace")) ||
-        (rc = dalloc(&op->wsB, 3 * nP, "operator workspace")))
-        return fail(rc);
     cudaError_t e = cudaDeviceSynchronize();
     dfree(stage);
     if (e != cudaSuccess) {
@@ -290,16 +287,31 @@ extern "C" int lp_operator_destroy(lp_operator *op) {
     for (int g = 0; g < op->n_beta_grids; ++g)
         if (op->beta_w[g]) dfree(op->beta_w[g]);
     if (op->alpha_w) dfree(op->alpha_w);
-    if (op->wsA) dfree(op->wsA);
-    if (op->wsB) dfree(op->wsB);
-    if (op->slab_grid) dfree(op->slab_grid);
+    for (int i = 0; i < op->nslabs; ++i) dfree(op->slabs[i].grid);
     delete op;
     return LP_OK;
 }
 
 namespace lp {
 
-int operator_apply(lp_operator *op, int which, const double *u, double *out, cudaStream_t st) {
+int64_t operator_ws_doubles(const lp_operator *op) { return 7 * op->nP; }
+
+static int operator_apply_ws(lp_operator *op, int which, const double *u, double *out,
+                             cudaStream_t st, double *ws);
+
+int operator_apply(lp_operator *op, int which, const double *u, double *out, cudaStream_t st,
+                   double *ws) {
+    if (ws) return operator_apply_ws(op, which, u, out, st, ws);
+    double *tmp = nullptr;
+    int rc = salloc(&tmp, (size_t)operator_ws_doubles(op), "operator workspace", st);
+    if (rc) return rc;
+    rc = operator_apply_ws(op, which, u, out, st, tmp);
+    sfree(tmp, st);
+    return rc;
+}
+
+static int operator_apply_ws(lp_operator *op, int which, const double *u, double *out,
+                             cudaStream_t st, double *ws) {
     const lp_plan *pl = op->plan;
     const LineTable &F = pl->tPhi, &D = pl->tDPhi;
     const int K = op->K, P = op->P, d = op->d;
@@ -307,8 +319,8 @@ int operator_apply(lp_operator *op, int which, const double *u, double *out, cud
     const bool hasB = (which & 2) != 0 && op->alpha_w != nullptr;
     const int64_t nP = op->nP;
     double *A[4], *B[3];
-    for (int i = 0; i < 4; ++i) A[i] = op->wsA + i * nP;
-    for (int i = 0; i < 3; ++i) B[i] = op->wsB + i * nP;
+    for (int i = 0; i < 4; ++i) A[i] = ws + i * nP;
+    for (int i = 0; i < 3; ++i) B[i] = ws + (4 + i) * nP;
     const int64_t nK = ipow(K, d);
     if (!hasA && !hasB) {
         LP_CUDA(cudaMemsetAsync(out, 0, nK * sizeof(double), st));

@@ -19,13 +19,23 @@ struct lp_operator {
     int n_beta_grids = 0;
     double *beta_w[3] = {nullptr, nullptr, nullptr};   // beta(x) w^d per diffusion direction
     double *alpha_w = nullptr;                         // alpha(x) w^d or null (B skipped)
-    double *wsA = nullptr, *wsB = nullptr;             // 4 and 3 fields of P^d
-    // slab-sharded middle stage (slab.cu): the coefficient grids of one y' slab,
-    // [4][P][ny][P], extracted on first use
-    double *slab_grid = nullptr;
-    int slab_y0 = -1, slab_ny = -1;
+    // slab-sharded middle stage (slab.cu): the coefficient grids of y' slabs,
+    // [4][P][ny][P] each, extracted on first use and kept (up to MAX_SLABS slabs,
+    // so a one-device emulation over several ranks does not re-extract)
+    static constexpr int MAX_SLABS = 8;
+    struct SlabGrid {
+        int y0 = -1, ny = -1;
+        double *grid = nullptr;
+    } slabs[MAX_SLABS];
+    int nslabs = 0;
 };
 
 namespace lp {
-int operator_apply(lp_operator *op, int which, const double *u, double *out, cudaStream_t st);
+// Doubles of workspace one apply needs (7 fields of P^d).
+int64_t operator_ws_doubles(const lp_operator *op);
+// apply_A / apply_B / apply_system.  ws: operator_ws_doubles(op) doubles of
+// device workspace, or null to take stream-ordered scratch for this call (the
+// handle is never written, so concurrent applies on different streams are safe).
+int operator_apply(lp_operator *op, int which, const double *u, double *out, cudaStream_t st,
+                   double *ws = nullptr);
 }

@@ -39,7 +39,7 @@ int copy2d(int64_t rows, int cols, const double *src, int64_t lds, double *dst, 
            cudaStream_t st) {
     if (rows <= 0 || cols <= 0) return LP_OK;
     int64_t blocks = ceil_div(rows * cols, 256);
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > num_sms() * 16) blocks = num_sms() * 16;
     copy2d_kernel<<<(unsigned)blocks, 256, 0, st>>>(rows, cols, src, lds, dst, ldd);
     count_launch();
     LP_CHECK_LAUNCH();
@@ -120,27 +120,42 @@ extern "C" int lp_slab_middle(lp_operator *op, int which, int y0, int ny, const 
     const size_t nq = (size_t)P * ny * P;   // [z'][ny][x']
     // the coefficient grids of the slab, in the S3 output layout [z'][y' - y0][x'],
     // extracted once per (operator, slab) and kept with the operator
-    if (op->slab_y0 != y0 || op->slab_ny != ny) {
-        if (op->slab_grid) dfree(op->slab_grid);
-        op->slab_grid = nullptr;
-        int rcg = dalloc(&op->slab_grid, 4 * nq, "slab grids");
-        if (rcg) return rcg;
+    lp_operator::SlabGrid *sg = nullptr;
+    for (int i = 0; i < op->nslabs; ++i)
+        if (op->slabs[i].y0 == y0 && op->slabs[i].ny == ny) sg = &op->slabs[i];
+    if (!sg) {
+        if (op->nslabs < lp_operator::MAX_SLABS) {
+            sg = &op->slabs[op->nslabs++];
+        } else {
+            // evict the oldest, stream-ordered after the work already queued on `st`
+            sg = &op->slabs[0];
+            dfree(sg->grid, st);
+            for (int i = 1; i < op->nslabs; ++i) op->slabs[i - 1] = op->slabs[i];
+            sg = &op->slabs[op->nslabs - 1];
+        }
+        sg->grid = nullptr;
+        sg->y0 = sg->ny = -1;
+        int rcg = salloc(&sg->grid, 4 * nq, "slab grids", st);
+        if (rcg) {
+            --op->nslabs;
+            return rcg;
+        }
         const double *src[4] = {op->beta_w[0], op->beta_w[1], op->beta_w[2], op->alpha_w};
         for (int g = 0; g < 4; ++g) {
             if (!src[g]) continue;
             // P planes z', each a block of ny rows of P at row offset y0
             for (int z = 0; z < P; ++z)
                 if ((rcg = copy2d(ny, P, src[g] + ((size_t)z * P + y0) * P, P,
-                                  op->slab_grid + g * nq + (size_t)z * ny * P, P, st)))
+                                  sg->grid + g * nq + (size_t)z * ny * P, P, st)))
                     return rcg;
         }
-        op->slab_y0 = y0;
-        op->slab_ny = ny;
+        sg->y0 = y0;
+        sg->ny = ny;
     }
     double *buf = nullptr;
     LP_CUDA(cudaMallocAsync((void **)&buf, 4 * nq * sizeof(double), st));
     double *q[4] = {buf, buf + nq, buf + 2 * nq, buf + 3 * nq};
-    double *gr[4] = {op->slab_grid, op->slab_grid + nq, op->slab_grid + 2 * nq, op->slab_grid + 3 * nq};
+    double *gr[4] = {sg->grid, sg->grid + nq, sg->grid + 2 * nq, sg->grid + 3 * nq};
     int rc = LP_OK;
     auto body = [&]() -> int {
         LtArgs s3 = lt_unfold(F, P * ny);

@@ -69,7 +69,8 @@ __global__ void sub_kernel(int64_t n, const double *__restrict__ f, const double
 
 unsigned grid_for(int64_t n) {
     int64_t b = ceil_div(n, 256);
-    return (unsigned)(b < 4 * 148 ? (b > 0 ? b : 1) : 4 * 148);
+    const int64_t cap = 4 * (int64_t)num_sms();
+    return (unsigned)(b < cap ? (b > 0 ? b : 1) : cap);
 }
 
 }  // namespace

@@ -218,14 +218,12 @@ def test_ilu0_and_sweeps_box(golden, name, N, T):
     assert relerr(precond_apply(f, g[k + "_r"]), g[k + "_z"]) < 1e-11
 
 
-@pytest.mark.parametrize("name,N,T", [c for c in PRE if c != ("cfg4", 12, 8)])
+@pytest.mark.parametrize("name,N,T", [c for c in PRE if c[0] in ("cfg1", "cfg2", "cfg3")])
 def test_ilu0_csr_bitwise(golden, name, N, T):
     """The general CSR kernel on the reference's own M reproduces its
     factors bit for bit (same k order, separately rounded mul/sub)."""
     g = golden("precond")
-    k = f"pc_{name}_N{N}_T{T}"
-    if k + "_values" not in g:
-        pytest.skip("M too large for a committed fixture")
+    k = f"pc_{name}_N{N}_T{T}"   # 3-D cases: test_ilu0_csr_bitwise_3d
     n = g[k + "_indptr"].size - 1
     m = SparseMatrix(n, g[k + "_indptr"], g[k + "_indices"], g[k + "_values"])
     f = ilu0(m)
