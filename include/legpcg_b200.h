@@ -117,6 +117,27 @@ int lp_copy2d(int64_t rows, int cols, const double *src, int64_t lds, double *ds
 int lp_sweep_ranks(lp_ilu *f, int nranks, const int *ys, int dir, const double *rhs,
                    int rhs_replicated, double *out, void *stream);
 
+/* One rank of the same sweep in a multi-GPU run (one process per GPU, every
+ * rank launching concurrently): only this rank's lines, in the global
+ * wavefront order.  out: this rank's replica (n values: the rank's own lines
+ * and the halo lines its neighbours store into it), pre-filled with
+ * lp_sweep_prefill BEFORE the ranks synchronise for the sweep (a neighbour's
+ * halo stores must land after the fill); rhs: this rank's replica of the
+ * right-hand side; peers[v]: rank v's
+ * replica mapped with lp_ipc_open (required for the slab neighbours rank-1 and
+ * rank+1; halo values are stored into it over NVLink with .sys-scope stores).
+ * Replaces, per rank, the forward_sub / backward_sub of sparse.py:199-216. */
+int lp_sweep_rank(lp_ilu *f, int nranks, const int *ys, int rank, int dir, const double *rhs,
+                  double *out, double *const *peers, void *stream);
+int lp_sweep_prefill(int64_t n, double *out, void *stream);
+
+/* CUDA IPC for the replicas: a cudaMalloc'd buffer and its 64-byte handle;
+ * mapping / unmapping a peer's handle. */
+int lp_ipc_alloc(int64_t bytes, void **ptr, unsigned char *handle64);
+int lp_ipc_free(void *ptr);
+int lp_ipc_open(const unsigned char *handle64, void **ptr);
+int lp_ipc_close(void *ptr);
+
 /* ----------------------------------------------------- preconditioner --
  * General CSR matrix (SparseMatrix, sparse.py:38-86): upload and hold.
  * indptr[n+1], indices[nnz] (sorted per row), values[nnz]; host or device. */

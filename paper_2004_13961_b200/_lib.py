@@ -67,6 +67,12 @@ _SIGS = {
     "lp_dot": (_i32, [_i64, _vp, _vp, _vp, _vp]),
     "lp_copy2d": (_i32, [_i64, _i32, _vp, _i64, _vp, _i64, _vp]),
     "lp_sweep_ranks": (_i32, [_vp, _i32, _vp, _i32, _vp, _i32, _vp, _vp]),
+    "lp_sweep_rank": (_i32, [_vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "lp_sweep_prefill": (_i32, [_i64, _vp, _vp]),
+    "lp_ipc_alloc": (_i32, [_i64, ctypes.POINTER(_vp), _vp]),
+    "lp_ipc_free": (_i32, [_vp]),
+    "lp_ipc_open": (_i32, [_vp, ctypes.POINTER(_vp)]),
+    "lp_ipc_close": (_i32, [_vp]),
     "lp_update_p": (_i32, [_i64, _vp, _vp, _dbl, _i32, _vp]),
     "lp_update_xr": (_i32, [_i64, _vp, _vp, _vp, _vp, _dbl, _vp, _vp]),
     "lp_slab_forward": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),

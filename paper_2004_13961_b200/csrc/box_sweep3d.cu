@@ -26,6 +26,7 @@
 // canonicalised.  The backward sweep is the mirror image (lines and rows in
 // reverse, the upper half of each row, division by the diagonal).
 #include <math.h>
+#include <string.h>
 
 #include <vector>
 
@@ -85,14 +86,21 @@ struct Sweep3Args {
     const int *order;            // ticket -> forward line index (wavefront order)
     const int *gpos;             // small reach: group g = lines order[gpos[g] .. gpos[g+1])
     int ngroups;
+    int nrun;                    // entries of `order` to process (plain kernel)
     // y-slab ranks: rank v owns the lines with y in [ys[v], ys[v+1]).
-    // Every rank keeps a replica of the vector (replica v at out + v * rep_stride,
-    // rhs likewise at rhs + v * rhs_stride); a line is read from and written to
-    // its owner's replica and also written to every rank whose stencil halo
-    // [ys[u] - r, ys[u+1] + r) contains it.  nranks = 1 is the plain sweep.
+    // Every rank keeps a replica of the vector (rep[v]; rhs in rhsrep[v]); a line
+    // is read from and written to its owner's replica and also written to every
+    // rank whose stencil halo [ys[u] - r, ys[u+1] + r) contains it.  In the
+    // one-launch emulation all replicas are slices of one device buffer and
+    // `order` holds every line; in a multi-GPU run each process launches its own
+    // lines only (`order` filtered to them) and the neighbours' replicas are
+    // peer (CUDA IPC) mappings, written over NVLink with .sys-scope stores and
+    // polled with .sys-scope loads (sys != 0).  nranks = 1 is the plain sweep.
     int nranks;
     int ys[MAX_RANKS + 1];
-    int64_t rep_stride, rhs_stride;
+    double *rep[MAX_RANKS];
+    const double *rhsrep[MAX_RANKS];
+    int sys;
     unsigned long long *trace;   // LP_SWEEP_TRACE: [nlines][8] (ticket time, rows 0 / K/4 / K/2 / K-1 done)
 };
 
@@ -126,8 +134,20 @@ __device__ __forceinline__ double canon3(double v) {
     return isnan(v) ? __longlong_as_double(0x7FF8000000000000ll) : v;
 }
 
-__device__ __forceinline__ double wait_value(const double *p, double v) {
-    while (is_sent(v)) v = ld_rel(p);
+__device__ __forceinline__ double ld_rel_sys(const double *p) {
+    double v;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// halo copy into a (possibly peer) replica
+__device__ __forceinline__ void st_halo(double *p, double v, bool sys, unsigned long long pol) {
+    if (sys) asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+    else asm volatile("st.relaxed.gpu.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ double wait_value(const double *p, double v, bool sys = false) {
+    while (is_sent(v)) v = sys ? ld_rel_sys(p) : ld_rel(p);
     return v;
 }
 
@@ -182,14 +202,14 @@ __global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_
         __syncthreads();
         const int t = sh_line;
         __syncthreads();
-        if (t >= nlines) return;
+        if (t >= a.nrun) return;
         const int L = FWD ? a.order[t] : nlines - 1 - a.order[t];
         const int ly = L % K, lz = L / K;
         const int64_t row0 = (int64_t)L * K;
         int owner = 0;
         while (owner + 1 < a.nranks && ly >= a.ys[owner + 1]) ++owner;
-        double *const out = a.out + owner * a.rep_stride;    // this line's replica
-        const double *const rhs = a.rhs + owner * a.rhs_stride;
+        double *const out = a.rep[owner];    // this line's replica
+        const double *const rhs = a.rhsrep[owner];
 #ifdef LP_SWEEP_TRACE
         if (tid == 0) a.trace[(size_t)t * 8] = gtime_s3();
 #endif
@@ -281,7 +301,7 @@ __global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_
 #endif
                     for (int v = 0; v < a.nranks; ++v)   // halo copies (multi-rank only)
                         if (v != owner && ly >= a.ys[v] - R && ly < a.ys[v + 1] + R)
-                            st_keep(a.out + v * a.rep_stride + i, y, pol_keep);
+                            st_halo(a.rep[v] + i, y, a.sys != 0, pol_keep);
 #pragma unroll
                     for (int d = R - 1; d >= 1; --d) h[d] = h[d - 1];
                     h[0] = y;
@@ -314,7 +334,7 @@ __global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_
             for (int j = 0; j < PR3; ++j) yr[j] = yq[j];
 #pragma unroll
             for (int pp = 0; pp < R; ++pp)
-                if (active && pp < K) win[pp % W] = wait_value(srcp(pp), win[pp % W]);
+                if (active && pp < K) win[pp % W] = wait_value(srcp(pp), win[pp % W], a.sys != 0);
             const int coff = ql * W;   // slot of (ox = -R) in this slot line, relative to `base`
             for (int u0 = 0; u0 < K; u0 += W) {
 #pragma unroll
@@ -334,7 +354,7 @@ __global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_
                             // has it, and only if both are empty does the thread spin.
                             double v = yq[k % P3];
                             if (is_sent(v)) v = yr[k % PR3];
-                            if (active && pp < K) v = wait_value(srcp(pp), v);
+                            if (active && pp < K) v = wait_value(srcp(pp), v, a.sys != 0);
                             win[(k + R) % W] = v;
                             yq[k % P3] = fetch(pp + P3);
                             yr[k % PR3] = fetch(pp + PR3);
@@ -490,7 +510,7 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
             for (int e = lane; e < cnt * K; e += 32) {
                 const int j = e / K, x = e - j * K;
                 const int L = line_of(j);
-                const double *rh = a.rhs + owner_of(L % K) * a.rhs_stride;
+                const double *rh = a.rhsrep[owner_of(L % K)];
                 rhs_s[j * K + x] = __ldcg(rh + (int64_t)L * K + x);
             }
             __syncwarp();
@@ -498,7 +518,7 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
             const int L = mine ? line_of(lane) : 0;
             const int ly = L % K;
             const int owner = owner_of(ly);
-            double *const out = a.out + owner * a.rep_stride;
+            double *const out = a.rep[owner];
             const int64_t row0 = (int64_t)L * K;
             double h[R];
 #pragma unroll
@@ -542,7 +562,7 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
                     st_keep(out + i, y, pol_keep);
                     for (int v = 0; v < a.nranks; ++v)
                         if (v != owner && ly >= a.ys[v] - R && ly < a.ys[v + 1] + R)
-                            st_keep(a.out + v * a.rep_stride + i, y, pol_keep);
+                            st_halo(a.rep[v] + i, y, a.sys != 0, pol_keep);
 #pragma unroll
                     for (int d = R - 1; d >= 1; --d) h[d] = h[d - 1];
                     h[0] = y;
@@ -557,7 +577,7 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
             const int L = j < cnt ? line_of(j) : 0;
             const int ly = L % K, lz = L / K;
             const bool active = j < cnt && q < NQ && ly + oy >= 0 && ly + oy < K && lz + oz >= 0 && lz + oz < K;
-            const double *out = a.out + owner_of(ly) * a.rep_stride;
+            const double *out = a.rep[owner_of(ly)];
             const double *src = out + (active ? (int64_t)(L + oy + (int64_t)K * oz) * K : 0);
             auto srcp = [&](int pp) { return src + (FWD ? pp : K - 1 - pp); };
             auto fetch = [&](int pp) {
@@ -572,7 +592,7 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
             for (int k = 0; k < P3; ++k) yq[k] = fetch(R + k);
 #pragma unroll
             for (int pp = 0; pp < R; ++pp)
-                if (active && pp < K) win[pp % W] = wait_value(srcp(pp), win[pp % W]);
+                if (active && pp < K) win[pp % W] = wait_value(srcp(pp), win[pp % W], a.sys != 0);
             const int coff = ql * W;
             const int64_t row0 = (int64_t)L * K;
             for (int u0 = 0; u0 < K; u0 += W) {
@@ -587,7 +607,7 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
                         {
                             const int pp = u + R;
                             double v = yq[k % P3];
-                            if (active && pp < K) v = wait_value(srcp(pp), v);
+                            if (active && pp < K) v = wait_value(srcp(pp), v, a.sys != 0);
                             win[(k + R) % W] = v;
                             yq[k % P3] = fetch(pp + P3);
                         }
@@ -643,7 +663,7 @@ int launch3(const Sweep3Args &a, cudaStream_t st) {
     auto kern = box_sweep3d_kernel<FWD, R>;
     const int nblocks = resident_blocks(reinterpret_cast<const void *>(kern), G::NT, smem);
     if (nblocks < 1) return LP_ERR_ARG;
-    int blocks = nblocks < a.g.nlines ? nblocks : a.g.nlines;
+    int blocks = nblocks < a.nrun ? nblocks : a.nrun;
     kern<<<blocks, G::NT, smem, st>>>(a);
     count_launch();
     LP_CHECK_LAUNCH();
@@ -734,6 +754,52 @@ static int small_reach_lpb(int r) {
     }
 }
 
+// Forward / backward line order of one rank of a y-slab split (lines of the
+// global wavefront order whose y -- mirrored for the backward sweep, which
+// walks order[] from the other end -- lies in the rank's slab), cached.
+static int rank_order(BoxLayout &b, const RankLayout &lay, bool fwd, int lpb, cudaStream_t st) {
+    BoxLayout::RankOrder &ro = b.rank_order[fwd ? 0 : 1];
+    int sig[11] = {lay.nranks, lay.own};
+    for (int v = 0; v <= lay.nranks; ++v) sig[2 + v] = lay.ys[v];
+    bool same = true;
+    for (int i = 0; i < 2 + lay.nranks + 1; ++i) same = same && ro.sig[i] == sig[i];
+    if (same && ro.order) return LP_OK;
+    const int K = b.K, A = b.r + 1;
+    std::vector<int> ord((size_t)K * K);
+    LP_CUDA(cudaMemcpy(ord.data(), b.line_order, ord.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    std::vector<int> mine, gp;
+    const int y0 = lay.ys[lay.own], y1 = lay.ys[lay.own + 1];
+    for (int o : ord) {
+        const int y = fwd ? o % K : K - 1 - o % K;
+        if (y >= y0 && y < y1) mine.push_back(o);
+    }
+    int prev_key = -1, run = 0;
+    for (size_t p = 0; p < mine.size(); ++p) {
+        const int key = mine[p] % K + A * (mine[p] / K);
+        if (key != prev_key || run == lpb) {
+            gp.push_back((int)p);
+            run = 0;
+            prev_key = key;
+        }
+        ++run;
+    }
+    gp.push_back((int)mine.size());
+    dfree(ro.order);
+    dfree(ro.groups);
+    ro.order = ro.groups = nullptr;
+    int rc;
+    if ((rc = dalloc(&ro.order, mine.size(), "rank line order")) ||
+        (rc = dalloc(&ro.groups, gp.size(), "rank line groups")))
+        return rc;
+    LP_CUDA(cudaMemcpy(ro.order, mine.data(), mine.size() * sizeof(int), cudaMemcpyHostToDevice));
+    LP_CUDA(cudaMemcpy(ro.groups, gp.data(), gp.size() * sizeof(int), cudaMemcpyHostToDevice));
+    ro.norder = (int)mine.size();
+    ro.ngroups = (int)gp.size() - 1;
+    for (int i = 0; i < 11; ++i) ro.sig[i] = i < 2 + lay.nranks + 1 ? sig[i] : -1;
+    (void)st;
+    return LP_OK;
+}
+
 // The caller has pre-filled `out` with the sentinel and reset the ticket.
 int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket, cudaStream_t st,
                 const RankLayout *ranks) {
@@ -746,22 +812,44 @@ int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket
     Sweep3Args a;
     a.g = g;
     a.lu = m->box.lu;
-    a.rhs = rhs;
-    a.out = out;
     a.ticket = ticket;
     a.order = m->box.line_order;
+    a.nrun = g.nlines;
     a.gpos = lpb ? m->box.line_groups : nullptr;
     a.ngroups = lpb ? m->box.n_line_groups : g.nlines;
     a.nranks = 1;
     a.ys[0] = 0;
     a.ys[1] = g.K;
-    a.rep_stride = 0;
-    a.rhs_stride = 0;
+    a.sys = 0;
+    for (int v = 0; v < MAX_RANKS; ++v) {
+        a.rep[v] = out;
+        a.rhsrep[v] = rhs;
+    }
     if (ranks && ranks->nranks > 1) {
         a.nranks = ranks->nranks;
         for (int v = 0; v <= a.nranks; ++v) a.ys[v] = ranks->ys[v];
-        a.rep_stride = g.n;
-        a.rhs_stride = ranks->rhs_replicated ? g.n : 0;
+        if (ranks->own < 0) {
+            for (int v = 0; v < a.nranks; ++v) {
+                a.rep[v] = out + (size_t)v * g.n;
+                a.rhsrep[v] = rhs + (ranks->rhs_replicated ? (size_t)v * g.n : 0);
+            }
+        } else {
+            for (int v = 0; v < a.nranks; ++v) a.rep[v] = v == ranks->own ? out : ranks->peers[v];
+            a.sys = 1;
+        }
+    }
+    if (ranks && ranks->own >= 0) {
+        RankLayout lay = *ranks;
+        if (lay.nranks == 1) {
+            lay.ys[0] = 0;
+            lay.ys[1] = g.K;
+        }
+        if ((rc = rank_order(m->box, lay, fwd, lpb ? lpb : 1, st))) return rc;
+        const BoxLayout::RankOrder &ro = m->box.rank_order[fwd ? 0 : 1];
+        a.order = ro.order;
+        a.nrun = ro.norder;
+        a.gpos = lpb ? ro.groups : nullptr;
+        a.ngroups = lpb ? ro.ngroups : ro.norder;
     }
     a.trace = nullptr;
 #ifdef LP_SWEEP_TRACE
@@ -825,3 +913,75 @@ extern "C" int lp_sweep_ranks(lp_ilu *f, int nranks, const int *ys, int dir, con
     return rc;
 }
 
+// Sentinel pre-fill of a replica (lp_sweep_rank's `out`): every rank fills its
+// replicas BEFORE the ranks synchronise (the neighbours' halo stores must not
+// be overwritten).
+extern "C" int lp_sweep_prefill(int64_t n, double *out, void *stream) {
+    fill_sent3<<<num_sms() * 8, 256, 0, as_stream(stream)>>>(n, out);
+    count_launch();
+    LP_CHECK_LAUNCH();
+    return LP_OK;
+}
+
+// One rank of a multi-GPU y-slab sweep: this process's lines
+// only, in the global wavefront order; out = this rank's replica (pre-filled
+// with lp_sweep_prefill before the ranks synchronise), peers[v] = the other ranks' replicas mapped through
+// lp_ipc_open (NULL for rank `rank` itself and for ranks whose slab is not
+// adjacent); rhs = this rank's replica of the right-hand side.  Every rank
+// launches concurrently (one GPU each); the line values a neighbour needs are
+// stored straight into its replica over NVLink.  Same arithmetic per line as
+// lp_forward_sub / lp_backward_sub.
+extern "C" int lp_sweep_rank(lp_ilu *f, int nranks, const int *ys, int rank, int dir,
+                             const double *rhs, double *out, double *const *peers, void *stream) {
+    LP_ARG(f->kind == MAT_BOX && f->factored, "lp_sweep_rank needs a factored box matrix");
+    Geom g = geom_of(f->box);
+    LP_ARG(box_sweep3d_applies(g), "lp_sweep_rank is for 3-D box factors (reach 2..10)");
+    LP_ARG(nranks >= 1 && nranks <= MAX_RANKS, "nranks must be in 1..%d", MAX_RANKS);
+    LP_ARG(rank >= 0 && rank < nranks, "rank %d outside [0, %d)", rank, nranks);
+    LP_ARG(ys[0] == 0 && ys[nranks] == g.K, "y slabs must cover [0, K)");
+    for (int v = 0; v < nranks; ++v) LP_ARG(ys[v] < ys[v + 1], "empty y slab");
+    for (int v = 0; v < nranks; ++v)
+        if (v != rank && (v == rank - 1 || v == rank + 1))
+            LP_ARG(peers && peers[v], "missing replica of neighbour rank %d", v);
+    cudaStream_t st = as_stream(stream);
+    RankLayout lay;
+    lay.nranks = nranks;
+    for (int v = 0; v <= nranks; ++v) lay.ys[v] = ys[v];
+    lay.own = rank;
+    for (int v = 0; v < nranks; ++v) lay.peers[v] = (peers && v != rank) ? peers[v] : nullptr;
+    int *tk = nullptr;
+    int rc;
+    if ((rc = salloc(&tk, 1, "sweep ticket", st))) return rc;
+    LP_CUDA(cudaMemsetAsync(tk, 0, sizeof(int), st));
+    rc = box_sweep3d(f, dir == 0, rhs, out, tk, st, &lay);
+    sfree(tk, st);
+    return rc;
+}
+
+// CUDA IPC plumbing for the replicas (one process per GPU).  lp_ipc_alloc:
+// cudaMalloc'd device buffer plus its 64-byte IPC handle; lp_ipc_open maps a
+// peer's handle (peer access over NVLink).
+extern "C" int lp_ipc_alloc(int64_t bytes, void **ptr, unsigned char *handle64) {
+    LP_CUDA(cudaMalloc(ptr, (size_t)bytes));
+    cudaIpcMemHandle_t h;
+    LP_CUDA(cudaIpcGetMemHandle(&h, *ptr));
+    memcpy(handle64, &h, sizeof h);
+    return LP_OK;
+}
+
+extern "C" int lp_ipc_free(void *ptr) {
+    LP_CUDA(cudaFree(ptr));
+    return LP_OK;
+}
+
+extern "C" int lp_ipc_open(const unsigned char *handle64, void **ptr) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof h);
+    LP_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return LP_OK;
+}
+
+extern "C" int lp_ipc_close(void *ptr) {
+    LP_CUDA(cudaIpcCloseMemHandle(ptr));
+    return LP_OK;
+}

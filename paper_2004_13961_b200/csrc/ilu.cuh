@@ -29,6 +29,13 @@ struct BoxLayout {
     int *line_order = nullptr;
     int *line_groups = nullptr;   // small reach: starts of same-key groups in line_order
     int n_line_groups = 0;
+    // one rank's lines of a y-slab split (multi-GPU sweeps): forward / backward
+    // wavefront orders filtered to the rank's lines, and their same-key groups
+    struct RankOrder {
+        int sig[11] = {-1};       // nranks, own, ys[0..nranks]
+        int *order = nullptr, *groups = nullptr;
+        int norder = 0, ngroups = 0;
+    } rank_order[2];
     // 2-D factorisation (ilu_box2d.cu): block tasks in key order, RN(1/u_ii) per row
     int *ilu_tasks = nullptr;
     int ilu_ntask = 0, ilu_nb = 0;
@@ -68,11 +75,16 @@ struct SweepScratch {
 };
 int scratch_alloc(const lp_ilu *m, SweepScratch &s, cudaStream_t st);
 void scratch_free(SweepScratch &s, cudaStream_t st);
-// 3-D sweeps with the vector distributed over y-slab ranks (lp_sweep_ranks)
+// 3-D sweeps with the vector distributed over y-slab ranks: own = -1 is the
+// one-launch emulation of every rank (replicas at out + v n, lp_sweep_ranks);
+// own >= 0 is one rank of a multi-GPU run (lp_sweep_rank): only its lines, its
+// replica `out`, the neighbours' replicas in peers[v] (IPC-mapped).
 struct RankLayout {
     int nranks = 1;
     int ys[9] = {0};
     bool rhs_replicated = false;
+    int own = -1;
+    double *peers[8] = {nullptr};
 };
 int ilu_apply(lp_ilu *m, const double *r, double *z, const SweepScratch &s, cudaStream_t st);
 int ilu_forward(lp_ilu *m, const double *r, double *y, const SweepScratch &s, cudaStream_t st);

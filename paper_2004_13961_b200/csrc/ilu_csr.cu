@@ -284,6 +284,10 @@ extern "C" int lp_ilu_destroy(lp_ilu *m) {
                     m->box.line_groups, m->box.full, m->box.ilu_tasks, m->box.rdiag};
     for (void *p : ptrs)
         if (p) dfree(p);
+    for (auto &ro : m->box.rank_order) {
+        dfree(ro.order);
+        dfree(ro.groups);
+    }
     delete m;
     return LP_OK;
 }

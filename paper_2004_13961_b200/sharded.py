@@ -247,6 +247,287 @@ class SlabSweeps:
         return out
 
 
+# ------------------------------------------------------------ PCG driver
+#
+# One PCG loop (pcg.py:145-164) written against per-slab operations, run either
+# by one process for all G ranks (LocalOps: the one-device emulation) or by
+# each process of a torch.distributed job for its own rank (RankOps).  Vectors
+# are lists of this process's z-slabs; dots are per-slab double-double partials
+# combined in rank order (a plain loop locally, ordered_dd_allreduce across
+# processes), so both paths produce the same bits.
+
+
+def pcg_loop(ops, config, f):
+    """Algorithm 1 over ops (this process's slabs).  Returns (x slabs, report)."""
+    import math
+    x = ops.zeros()
+    r = ops.copy(f)
+    p = ops.empty()
+    fnorm = math.sqrt(ops.dot(f, f))
+    rr = ops.dot(r, r)
+    hist = [math.sqrt(rr)]
+    tol = config.epsilon * fnorm
+    it, rho_old = 0, None
+    while math.sqrt(rr) > tol and it < config.k_max:
+        z = ops.precond(r)
+        it += 1
+        rho = ops.dot(r, z)
+        beta = 0.0 if it == 1 else rho / rho_old
+        ops.update_p(z, p, beta, it == 1)
+        w = ops.matvec(p)
+        curv = ops.dot(p, w)
+        if curv <= 0.0:
+            from .pcg import IndefiniteOperatorError
+            raise IndefiniteOperatorError(it, curv)
+        rr = ops.update_xr(x, r, p, w, rho / curv)
+        rho_old = rho
+        hist.append(math.sqrt(rr))
+    return x, {"iterations": it, "converged": math.sqrt(rr) <= tol,
+               "final_relative_residual": math.sqrt(rr) / fnorm if fnorm else 0.0,
+               "residual_history": hist, "ranks": ops.G}
+
+
+class _GpuSlabOps:
+    """Per-slab vector kernels (lp_dot, lp_update_p, lp_update_xr) on CUDA slabs."""
+
+    def __init__(self, K, G, sizes):
+        import torch
+        self.torch = torch
+        self.lib = _lib.load()
+        self.K, self.G = K, G
+        self.sizes = sizes                          # this process's slab lengths
+        self._two = torch.empty(2, dtype=torch.float64, device="cuda")
+
+    def _new(self):
+        return [self.torch.empty(max(c, 1), dtype=self.torch.float64, device="cuda")[:c]
+                for c in self.sizes]
+
+    def zeros(self):
+        return [t.zero_() for t in self._new()]
+
+    def empty(self):
+        return self._new()
+
+    def copy(self, v):
+        return [t.clone() for t in v]
+
+    def _partial(self, a, b):
+        _lib.check(self.lib.lp_dot(a.numel(), a.data_ptr(), b.data_ptr(), self._two.data_ptr(),
+                                   _lib.stream_ptr()), "dot")
+        h = self._two.cpu().numpy()
+        return float(h[0]), float(h[1])
+
+    def dot(self, a, b):
+        return self.combine([self._partial(u, v) for u, v in zip(a, b)])[0]
+
+    def update_p(self, z, p, beta, first):
+        for zs, ps in zip(z, p):
+            _lib.check(self.lib.lp_update_p(zs.numel(), zs.data_ptr(), ps.data_ptr(), beta,
+                                            int(first), _lib.stream_ptr()), "update p")
+
+    def update_xr(self, x, r, p, w, alpha):
+        parts = []
+        for xs, rs, ps, ws in zip(x, r, p, w):
+            _lib.check(self.lib.lp_update_xr(xs.numel(), xs.data_ptr(), rs.data_ptr(), ps.data_ptr(),
+                                             ws.data_ptr(), alpha, self._two.data_ptr(),
+                                             _lib.stream_ptr()), "update x r")
+            h = self._two.cpu().numpy()
+            parts.append((float(h[0]), float(h[1])))
+        return self.combine(parts)[0]
+
+
+class LocalOps(_GpuSlabOps):
+    """All G ranks in this process on one device (exchanges as device copies,
+    the sweeps' halo publication in one launch, lp_sweep_ranks)."""
+
+    def __init__(self, spec, plan, G, factors):
+        K = spec.n_modes
+        super().__init__(K, G, [nz * K * K for _, nz in slab_bounds(K, G)])
+        self.sm = SlabMatvec(spec, plan, G)
+        self.sw = SlabSweeps(factors, K, G) if factors is not None else None
+
+    def combine(self, parts):
+        acc = (0.0, 0.0)
+        for pr in parts:
+            acc = _dd_add(acc, pr)
+        return acc
+
+    def matvec(self, p):
+        return [o[:c] for o, c in zip(self.sm.apply_local(p), self.sizes)]
+
+    def precond(self, r):
+        if self.sw is None:
+            return r
+        z = self.sw.apply(self.torch.cat(r))
+        return SlabMatvec.split(z, self.sizes)
+
+
+class RankSweeps:
+    """The ILU(0) sweeps of one rank of a multi-GPU run: the residual's
+    z-slab -> y-slab redistribution (one all-to-all), the forward and backward
+    sweeps over this rank's y-slab lines with halo lines stored straight into
+    the neighbours' replicas (lp_sweep_rank, CUDA IPC peer mappings), and the
+    y-slab -> z-slab redistribution of z (one all-to-all).
+
+    Replicas are full-length vectors (n values) addressed by global row; only
+    the rank's own lines and its +-r halo lines are meaningful.  Per iteration
+    a rank sends and receives (G-1)/G of its z-slab twice (r and z) and, during
+    each sweep, r K values per plane to each neighbour (the halo lines)."""
+
+    def __init__(self, factors, K, G, rank, group=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.ctypes = torch, dist, ctypes
+        self.f, self.K, self.G, self.rank, self.group = factors, K, G, rank, group
+        self.z = slab_bounds(K, G)
+        self.y = slab_bounds(K, G)
+        self.ys = [y0 for y0, _ in self.y] + [K]
+        self.n = K ** 3
+        self._setup()
+
+    # ------------------------------------------------------ device hooks
+    def _setup(self):
+        ctypes = self.ctypes
+        self.lib = _lib.load()
+        self._ys = (ctypes.c_int * (self.G + 1))(*self.ys)
+        # replicas: rhs (r, own lines), forward output y, backward output z
+        self.bufs, handles = [], []
+        for _ in range(3):
+            ptr = ctypes.c_void_p()
+            h = (ctypes.c_ubyte * 64)()
+            _lib.check(self.lib.lp_ipc_alloc(8 * self.n, ctypes.byref(ptr), h), "ipc alloc")
+            self.bufs.append(ptr.value)
+            handles.append(bytes(h))
+        allh = [None] * self.G
+        self.dist.all_gather_object(allh, handles, group=self.group)
+        self.peers = []   # [buffer][rank] -> mapped pointer (own: local buffer)
+        self._opened = []
+        for b in range(3):
+            row = (ctypes.c_void_p * self.G)()
+            for v in range(self.G):
+                if v == self.rank:
+                    row[v] = self.bufs[b]
+                elif abs(v - self.rank) == 1:
+                    p = ctypes.c_void_p()
+                    hb = (ctypes.c_ubyte * 64).from_buffer_copy(allh[v][b])
+                    _lib.check(self.lib.lp_ipc_open(hb, ctypes.byref(p)), "ipc open")
+                    row[v] = p.value
+                    self._opened.append(p.value)
+            self.peers.append(row)
+
+    def close(self):
+        for p in self._opened:
+            self.lib.lp_ipc_close(p)
+        for p in self.bufs:
+            self.lib.lp_ipc_free(p)
+        self._opened, self.bufs = [], []
+
+    def _empty(self, n):
+        return self.torch.empty(max(n, 1), dtype=self.torch.float64, device="cuda")
+
+    @staticmethod
+    def _addr(buf, off):
+        return (buf if isinstance(buf, int) else buf.data_ptr()) + 8 * off
+
+    def _copy2d(self, rows, cols, src, soff, lds, dst, doff, ldd):
+        _lib.check(self.lib.lp_copy2d(rows, cols, self._addr(src, soff), lds, self._addr(dst, doff),
+                                      ldd, _lib.stream_ptr()), "copy2d")
+
+    def _prefill(self):
+        # both output replicas hold the sentinel before any rank starts sweeping
+        st = _lib.stream_ptr()
+        for b in self.bufs[1:]:
+            _lib.check(self.lib.lp_sweep_prefill(self.n, b, st), "prefill")
+
+    def _sweeps(self):
+        lib, h, st = self.lib, self.f._handle, _lib.stream_ptr()
+        rrep, yrep, zrep = self.bufs
+        _lib.check(lib.lp_sweep_rank(h, self.G, self._ys, self.rank, 0, rrep, yrep, self.peers[1],
+                                     st), "forward sweep")
+        _lib.check(lib.lp_sweep_rank(h, self.G, self._ys, self.rank, 1, yrep, zrep, self.peers[2],
+                                     st), "backward sweep")
+
+    # ------------------------------------------------------------ schedule
+    def _exchange(self, send, send_sizes, recv_sizes):
+        recv = self._empty(sum(recv_sizes))
+        self.dist.all_to_all_single(recv[:sum(recv_sizes)], send[:sum(send_sizes)],
+                                    output_split_sizes=recv_sizes, input_split_sizes=send_sizes,
+                                    group=self.group)
+        return recv
+
+    def apply(self, r_slab):
+        """z = M^-1 r on this rank's z-slab of r (x fastest); returns its z-slab of z."""
+        K, me = self.K, self.rank
+        nz = self.z[me][1]
+        y0, ny = self.y[me]
+        rrep, zrep = self.bufs[0], self.bufs[2]
+        self._prefill()
+        # z -> y: to rank h the rows (my planes, h's lines): [nz][ny_h][K]
+        send_sizes = [nz * nyh * K for _, nyh in self.y]
+        recv_sizes = [nzg * ny * K for _, nzg in self.z]
+        send = self._empty(sum(send_sizes))
+        o = 0
+        for (yh, nyh), c in zip(self.y, send_sizes):
+            if c:
+                self._copy2d(nz, nyh * K, r_slab, yh * K, K * K, send, o, nyh * K)
+            o += c
+        recv = self._exchange(send, send_sizes, recv_sizes)
+        o = 0
+        for (zg, nzg), c in zip(self.z, recv_sizes):
+            if c:
+                self._copy2d(nzg, ny * K, recv, o, ny * K, rrep, (zg * K + y0) * K, K * K)
+            o += c
+        self._sweeps()
+        # y -> z: to rank g my lines of its planes: [nz_g][ny][K]
+        send_sizes, recv_sizes = recv_sizes, send_sizes
+        send = self._empty(sum(send_sizes))
+        o = 0
+        for (zg, nzg), c in zip(self.z, send_sizes):
+            if c:
+                self._copy2d(nzg, ny * K, zrep, (zg * K + y0) * K, K * K, send, o, ny * K)
+            o += c
+        recv = self._exchange(send, send_sizes, recv_sizes)
+        z = self._empty(nz * K * K)[:nz * K * K]
+        o = 0
+        for (yh, nyh), c in zip(self.y, recv_sizes):
+            if c:
+                self._copy2d(nz, nyh * K, recv, o, nyh * K, z, yh * K, K * K)
+            o += c
+        return z
+
+
+class RankOps(_GpuSlabOps):
+    """This process's rank of a torch.distributed job (one GPU per rank):
+    z-slab matvec with three NCCL all-to-alls, y-slab sweeps with peer halo
+    stores, dots combined with ordered_dd_allreduce."""
+
+    def __init__(self, spec, plan, factors, rank, G, group=None):
+        K = spec.n_modes
+        super().__init__(K, G, [slab_bounds(K, G)[rank][1] * K * K])
+        self.rank, self.group = rank, group
+        self.sm = SlabMatvec(spec, plan, G)
+        self.sw = RankSweeps(factors, K, G, rank, group) if factors is not None else None
+
+    def combine(self, parts):
+        from .distributed import ordered_dd_allreduce
+        acc = (0.0, 0.0)
+        for pr in parts:
+            acc = _dd_add(acc, pr)
+        return ordered_dd_allreduce(acc[0], acc[1], device="cuda")
+
+    def matvec(self, p):
+        return [self.sm.apply_rank(self.rank, p[0], self.group)[:self.sizes[0]]]
+
+    def precond(self, r):
+        return [self.sw.apply(r[0])] if self.sw is not None else r
+
+    def close(self):
+        if self.sw is not None:
+            self.sw.close()
+
+
 def pcg_solve_sharded_local(spec, config, plan, f_flat, G, factors=None):
     """PCG (pcg.py:111-179) with every stage distributed over G ranks, emulated
     on one device: the matvec z-slab sharded (SlabMatvec, three all-to-alls),
@@ -254,67 +535,29 @@ def pcg_solve_sharded_local(spec, config, plan, f_flat, G, factors=None):
     updates per z-slab (lp_update_p / lp_update_xr) and the three dots per
     iteration as per-slab double-double partials combined in rank order (what
     ordered_dd_allreduce does across processes).  Returns (x_full, report)."""
-    import math
-
     import torch
     from .pcg import setup_preconditioner
-    lib = _lib.load()
-    K = spec.n_modes
-    n = K ** 3
-    sm = SlabMatvec(spec, plan, G)
     if factors is None:
         factors = setup_preconditioner(spec, config, plan)
-    sw = SlabSweeps(factors, K, G) if factors is not None else None
-    zb = slab_bounds(K, G)
-    cut = [(z0 * K * K, nz * K * K) for z0, nz in zb]
-    st = _lib.stream_ptr
-    two = torch.empty(2, dtype=torch.float64, device="cuda")
+    ops = LocalOps(spec, plan, G, factors)
+    x, rep = pcg_loop(ops, config, SlabMatvec.split(f_flat, ops.sizes))
+    return torch.cat(x), rep
 
-    def dot(a, b):
-        """sum over ranks (rank order) of per-slab double-double a.b"""
-        acc = (0.0, 0.0)
-        for o, c in cut:
-            _lib.check(lib.lp_dot(c, a.data_ptr() + 8 * o, b.data_ptr() + 8 * o, two.data_ptr(), st()))
-            h = two.cpu().numpy()
-            acc = _dd_add(acc, (float(h[0]), float(h[1])))
-        return acc[0]
 
-    def matvec(u):
-        outs = sm.apply_local([u[o:o + c] for o, c in cut])
-        return torch.cat([w[:c] for w, (o, c) in zip(outs, cut)])
-
-    x = torch.zeros(n, dtype=torch.float64, device="cuda")
-    r = f_flat.clone()
-    p = torch.empty_like(r)
-    fnorm = math.sqrt(dot(f_flat, f_flat))
-    rr = dot(r, r)
-    hist = [math.sqrt(rr)]
-    tol = config.epsilon * fnorm
-    it, rho_old = 0, None
-    while math.sqrt(rr) > tol and it < config.k_max:
-        z = sw.apply(r) if sw is not None else r
-        it += 1
-        rho = dot(r, z)
-        beta = 0.0 if it == 1 else rho / rho_old
-        for o, c in cut:
-            _lib.check(lib.lp_update_p(c, z.data_ptr() + 8 * o, p.data_ptr() + 8 * o, beta,
-                                       int(it == 1), st()))
-        w = matvec(p)
-        curv = dot(p, w)
-        if curv <= 0.0:
-            from .pcg import IndefiniteOperatorError
-            raise IndefiniteOperatorError(it, curv)
-        alpha = rho / curv
-        acc = (0.0, 0.0)
-        for o, c in cut:
-            _lib.check(lib.lp_update_xr(c, x.data_ptr() + 8 * o, r.data_ptr() + 8 * o,
-                                        p.data_ptr() + 8 * o, w.data_ptr() + 8 * o, alpha,
-                                        two.data_ptr(), st()))
-            h = two.cpu().numpy()
-            acc = _dd_add(acc, (float(h[0]), float(h[1])))
-        rr = acc[0]
-        rho_old = rho
-        hist.append(math.sqrt(rr))
-    return x, {"iterations": it, "converged": math.sqrt(rr) <= tol,
-               "final_relative_residual": math.sqrt(rr) / fnorm if fnorm else 0.0,
-               "residual_history": hist, "ranks": G}
+def pcg_solve_sharded_rank(spec, config, plan, f_slab, factors=None, group=None):
+    """One rank of the distributed PCG under torch.distributed (torchrun, one
+    GPU per rank, NCCL): f_slab is this rank's z-slab of F (x fastest);
+    returns (this rank's z-slab of x, report).  Every rank factors M itself
+    (the factors are replicated; each rank's sweeps read only its own lines)."""
+    import torch.distributed as dist
+    from .pcg import setup_preconditioner
+    G = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if factors is None:
+        factors = setup_preconditioner(spec, config, plan)
+    ops = RankOps(spec, plan, factors, rank, G, group)
+    try:
+        x, rep = pcg_loop(ops, config, [f_slab])
+    finally:
+        ops.close()
+    return x[0], rep

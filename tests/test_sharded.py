@@ -169,6 +169,170 @@ def test_gloo_two_ranks_sharded_matvec():
     assert np.array_equal(got, local)
 
 
+# ------------------------------------------------ distributed PCG (numpy stand-ins)
+
+from paper_2004_13961_b200.distributed import dd_add, dd_of  # noqa: E402
+from paper_2004_13961_b200.sharded import RankSweeps, SlabMatvec, pcg_loop  # noqa: E402
+
+
+class _NumpyVecOps:
+    """Per-slab vector operations on CPU tensors with sequential double-double
+    dots (a stand-in for lp_dot / lp_update_p / lp_update_xr)."""
+
+    def zeros(self):
+        return [torch.zeros(c, dtype=torch.float64) for c in self.sizes]
+
+    def empty(self):
+        return [torch.empty(c, dtype=torch.float64) for c in self.sizes]
+
+    def copy(self, v):
+        return [t.clone() for t in v]
+
+    def dot(self, a, b):
+        return self.combine([dd_of((u * v).numpy()) for u, v in zip(a, b)])[0]
+
+    def update_p(self, z, p, beta, first):
+        for zs, ps in zip(z, p):
+            ps.copy_(zs if first else zs + beta * ps)
+
+    def update_xr(self, x, r, p, w, alpha):
+        for xs, rs, ps, ws in zip(x, r, p, w):
+            xs.add_(alpha * ps)
+            rs.sub_(alpha * ws)
+        return self.combine([dd_of((rs * rs).numpy()) for rs in r])[0]
+
+
+def _oracle_precond(spec, T):
+    fac = orc.ilu0(orc.assemble_M(spec, T, T))
+    return lambda r: torch.from_numpy(np.asarray(orc.precond_apply(fac, r.numpy()), dtype=np.float64))
+
+
+class NumpyLocalOps(_NumpyVecOps):
+    def __init__(self, spec, T, G):
+        K = spec.n_modes
+        self.G = G
+        self.sizes = [nz * K * K for _, nz in slab_bounds(K, G)]
+        self.sm = _numpy_slab(spec, G)
+        self.pre = _oracle_precond(spec, T)
+
+    def combine(self, parts):
+        acc = (0.0, 0.0)
+        for pr in parts:
+            acc = dd_add(acc, pr)
+        return acc
+
+    def matvec(self, p):
+        return [o[:c] for o, c in zip(self.sm.apply_local(p), self.sizes)]
+
+    def precond(self, r):
+        return SlabMatvec.split(self.pre(torch.cat(r)), self.sizes)
+
+
+class NumpyRankSweeps(RankSweeps):
+    """RankSweeps' redistribution schedule on CPU tensors; the sweeps themselves
+    by the oracle on the rank-summed residual (each rank contributes its lines)."""
+
+    def _setup(self):
+        self.bufs = [torch.zeros(self.n, dtype=torch.float64) for _ in range(3)]
+
+    def close(self):
+        pass
+
+    def _empty(self, n):
+        return torch.empty(max(n, 1), dtype=torch.float64)
+
+    def _copy2d(self, rows, cols, src, soff, lds, dst, doff, ldd):
+        s = src[soff:soff + (rows - 1) * lds + cols].as_strided((rows, cols), (lds, 1))
+        d = dst[doff:doff + (rows - 1) * ldd + cols].as_strided((rows, cols), (ldd, 1))
+        d.copy_(s)
+
+    def _prefill(self):
+        for b in self.bufs:
+            b.zero_()
+
+    def _sweeps(self):
+        r = self.bufs[0].clone()
+        self.dist.all_reduce(r)            # each rank placed only its own lines
+        self.bufs[2].copy_(self.pre(r))
+
+
+class NumpyRankOps(_NumpyVecOps):
+    def __init__(self, spec, T, rank, G):
+        K = spec.n_modes
+        self.G, self.rank = G, rank
+        self.sizes = [slab_bounds(K, G)[rank][1] * K * K]
+        self.sm = _numpy_slab(spec, G)
+        self.sw = NumpyRankSweeps(None, K, G, rank)
+        self.sw.pre = _oracle_precond(spec, T)
+
+    def combine(self, parts):
+        from paper_2004_13961_b200.distributed import ordered_dd_allreduce
+        acc = (0.0, 0.0)
+        for pr in parts:
+            acc = dd_add(acc, pr)
+        return ordered_dd_allreduce(*acc)
+
+    def matvec(self, p):
+        return [self.sm.apply_rank(self.rank, p[0])[:self.sizes[0]]]
+
+    def precond(self, r):
+        return [self.sw.apply(r[0])]
+
+
+def _pcg_problem(N=9, T=1):
+    from types import SimpleNamespace
+    from paper_2004_13961_b200 import SolverConfig
+    w = wl.cfg5()
+    spec = spec_of(w, N)
+    K = N - 1
+    F = wl.mass_contract_series(wl.seeded_fhat(3, N + 1))
+    f = np.ascontiguousarray(F.transpose(2, 1, 0)).reshape(-1)           # x fastest
+    return spec, f, SolverConfig(epsilon=1e-10, preconditioner=(T, T)), K
+
+
+def _pcg_worker(rank, ws, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(ws),
+                      RANK=str(rank), LOCAL_RANK=str(rank))
+    from paper_2004_13961_b200 import distributed as Dm
+    dist = Dm.init("gloo")
+    try:
+        spec, f, cfg, K = _pcg_problem()
+        ops = NumpyRankOps(spec, 1, rank, ws)
+        mine = _slabs(f, K, ws)[rank]
+        x, rep = pcg_loop(ops, cfg, [mine])
+        out[rank] = (x[0].numpy().tobytes(), rep["iterations"], rep["residual_history"])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_two_ranks_distributed_pcg():
+    """The per-rank PCG driver (pcg_loop over RankOps' schedule: z->y and y->z
+    redistributions around the sweeps, three all-to-alls per matvec, rank-ordered
+    dots) on two gloo processes with numpy stand-ins for the kernels is bit
+    for bit the single-process emulation over the same two slabs, and solves
+    the system like the CPU oracle."""
+    ws = 2
+    port = _free_port()
+    import torch.multiprocessing as mp
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_pcg_worker, args=(ws, port, out), nprocs=ws, join=True)
+        res = dict(out)
+    got = np.concatenate([np.frombuffer(res[r][0], dtype=np.float64) for r in range(ws)])
+    assert res[0][1] == res[1][1] and res[0][2] == res[1][2]
+    spec, f, cfg, K = _pcg_problem()
+    xl, rl = pcg_loop(NumpyLocalOps(spec, 1, ws), cfg, _slabs(f, K, ws))
+    assert np.array_equal(got, torch.cat(xl).numpy())
+    assert res[0][1] == rl["iterations"] and res[0][2] == rl["residual_history"]
+    # and the oracle's own PCG (x-fastest flat -> [x][y][z])
+    F = f.reshape(K, K, K).transpose(2, 1, 0)
+    xo, ro = orc.pcg_solve(spec, F, epsilon=cfg.epsilon, preconditioner=cfg.preconditioner)
+    xo_flat = np.ascontiguousarray(np.asarray(xo).transpose(2, 1, 0)).reshape(-1)
+    assert abs(ro["iterations"] - rl["iterations"]) <= 1
+    assert relerr(got, xo_flat) < 1e-10
+
+
 # ----------------------------------------------------------------------- GPU
 
 @pytest.mark.gpu
@@ -254,6 +418,35 @@ def test_sharded_pcg_matches_single_gpu(name, N, T, G):
         xo, ro = orc.pcg_solve(spec, F, epsilon=w.rtol, preconditioner=(T, T))
         assert abs(rg["iterations"] - ro["iterations"]) <= 1
         assert relerr(xg.cpu().numpy(), np.asarray(xo).flatten(order="F")) < 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,N,T", [("cfg5", 20, 1), ("cfg4", 14, 8)])
+def test_rank_pcg_one_rank_nccl_bit_identical(name, N, T):
+    """pcg_solve_sharded_rank -- the per-process driver of a multi-GPU run (NCCL
+    all-to-alls, IPC replicas, lp_sweep_rank, ordered allreduce) -- as a
+    one-rank NCCL job on this GPU is bit for bit the single-process emulation."""
+    import torch.distributed as dist
+    from paper_2004_13961_b200 import SolverConfig, TransformPlan, device
+    from paper_2004_13961_b200.pcg import setup_preconditioner
+    from paper_2004_13961_b200.sharded import pcg_solve_sharded_local, pcg_solve_sharded_rank
+    w = wl.CONFIGS[name]()
+    spec = spec_of(w, N)
+    plan = TransformPlan(N + 1)
+    cfg = SolverConfig(epsilon=w.rtol, preconditioner=(T, T))
+    F = wl.mass_contract_series(wl.seeded_fhat(3, N + 1))
+    fd = device.to_device(F.flatten(order="F"))
+    fac = setup_preconditioner(spec, cfg, plan)
+    xl, rl = pcg_solve_sharded_local(spec, cfg, plan, fd, 1, factors=fac)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0,
+                            world_size=1)
+    try:
+        xr, rr = pcg_solve_sharded_rank(spec, cfg, plan, fd, factors=fac)
+    finally:
+        dist.destroy_process_group()
+    assert rr["iterations"] == rl["iterations"]
+    assert rr["residual_history"] == rl["residual_history"]
+    assert torch.equal(xr, xl)
 
 
 @pytest.mark.gpu
