@@ -8,6 +8,7 @@ import sys
 from collections import defaultdict
 
 tag = sys.argv[1]
+wl = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].endswith(".ncu-rep") else "cfg3"
 src = "gpurun_out/"
 
 
@@ -38,7 +39,7 @@ for r in rows[1:]:
     raw.append((name, ms))
 tot = sum(v[1] for v in per.values())
 with open(f"profiles/{tag}_launches_summary.csv", "w") as f:
-    f.write(f"# {tag} launch list: `python bench.py --steps 1 --warmup 1 --no-cpu-baseline` under\n")
+    f.write(f"# {tag} launch list: `python bench.py --workload {wl} --steps 1 --warmup 1 --no-cpu-baseline` under\n")
     f.write("# `ncu --metrics gpu__time_duration.sum --clock-control none` (cold-cache, serialised: compare shares)\n")
     f.write("kernel,launches,total_ms,share\n")
     for name, (n, ms) in sorted(per.items(), key=lambda kv: -kv[1][1]):
@@ -54,26 +55,26 @@ keep = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "smsp__inst_executed.sum", "lts__t_bytes.sum",
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"]
-for name in ("sweep", "ilu", "mv"):
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct"]
+for name in ("sweep", "ilu", "matvec"):
     rows = table(src + f"prof_{name}_full.csv")
     if not rows:
         continue
     hdr = rows[0]
     cols = ["Kernel Name"] + [k for k in keep if k in hdr]
     idx = [hdr.index(c) for c in cols]
-    with open(f"profiles/{tag}_{name}_full.csv", "w") as f:
+    with open(f"profiles/{tag}_{wl}_{name}_full.csv", "w") as f:
         f.write(f"# ncu --set full --clock-control none --page raw, launches of the {name} kernel inside "
-                "python bench.py --steps 1 --warmup 1 (cfg 2)\n")
+                f"python bench.py --workload {wl} --steps 1 --warmup 1\n")
         w = csv.writer(f)
         w.writerow(cols)
         w.writerow([rows[1][i] for i in idx])   # units row
         for r in rows[2:]:
             w.writerow([r[i] for i in idx])
 print(open(f"profiles/{tag}_launches_summary.csv").read())
-for name in ("sweep", "ilu", "mv"):
+for name in ("sweep", "ilu", "matvec"):
     try:
-        print(open(f"profiles/{tag}_{name}_full.csv").read())
+        print(open(f"profiles/{tag}_{wl}_{name}_full.csv").read())
     except FileNotFoundError:
         pass
 
@@ -98,8 +99,8 @@ def summarize_rep(rep, out, note):
     print(open(f"profiles/{out}").read())
 
 
-if len(sys.argv) > 2:
+if len(sys.argv) > 3:
     # extra captures: <rep> <out.csv> <note>, repeated
-    extra = sys.argv[2:]
+    extra = sys.argv[3:]
     for k in range(0, len(extra) - 2, 3):
         summarize_rep(extra[k], extra[k + 1], extra[k + 2])
