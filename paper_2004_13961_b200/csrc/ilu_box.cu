@@ -142,23 +142,30 @@ __global__ void box_mask_kernel(Geom g, double *vals, uint32_t *mask,
 constexpr int ASM_RB = 32;
 constexpr int ASM_MAXJ = 8;   // parity-matched degrees per group in registers (tmax <= 15)
 
-__global__ void __launch_bounds__(256)
+// NG groups, J parity-matched degrees per group (t = (ox & 1) + 2j, j < J):
+// H is stored [slot-line][group][2J] with zeros past the group's degree and
+// each lane's X values past its degree are zero, so every entry is the same
+// unpredicated chain of NG * J FMAs (an x 0 term leaves the sum unchanged;
+// the mirror entry runs the same chain, so M stays exactly symmetric).
+template <int NG, int J>
+__global__ void __launch_bounds__(256, 2)
 box_assemble_kernel(const __grid_constant__ AsmArgs a, double *__restrict__ vals,
                     uint32_t *__restrict__ mask, unsigned char *__restrict__ full,
                     unsigned long long *nnz, unsigned long long *missing) {
     extern __shared__ __align__(16) double sm[];
+    constexpr int HT = 2 * J;
     const Geom &g = a.g;
-    const int nsl = g.d == 1 ? 1 : (g.d == 2 ? g.W : g.W * g.W);
-    const int TL = a.tmax + 1, NG = a.ngroups;
-    double *H = sm;   // [nsl][NG][TL]
-    uint32_t *mk = reinterpret_cast<uint32_t *>(H + (size_t)nsl * NG * TL);   // [ASM_RB][mw]
+    const int W = g.W, r = g.r;
+    const int nsl = g.d == 1 ? 1 : (g.d == 2 ? W : W * W);
+    double *H = sm;   // [nsl][NG][HT]
+    uint32_t *mk = reinterpret_cast<uint32_t *>(H + (size_t)nsl * NG * HT);   // [ASM_RB][mw]
     const int line = blockIdx.x;
     const int iy = g.d > 1 ? line % g.K : 0, iz = g.d > 2 ? line / g.K : 0;
     const int x0 = blockIdx.y * ASM_RB;
     const int nrows = min(ASM_RB, g.K - x0);
-    for (int q = threadIdx.x; q < nsl * NG * TL; q += blockDim.x) {
-        const int t = q % TL, gi = (q / TL) % NG, sl = q / (TL * NG);
-        const int oy = g.d > 1 ? sl % g.W - g.r : 0, oz = g.d > 2 ? sl / g.W - g.r : 0;
+    for (int q = threadIdx.x; q < nsl * NG * HT; q += blockDim.x) {
+        const int t = q % HT, gi = (q / HT) % NG, sl = q / (HT * NG);
+        const int oy = g.d > 1 ? sl % W - r : 0, oz = g.d > 2 ? sl / W - r : 0;
         const GroupDesc &G = a.grp[gi];
         double h = 0.0;
         if (t < G.lens[0]) {
@@ -176,47 +183,44 @@ box_assemble_kernel(const __grid_constant__ AsmArgs a, double *__restrict__ vals
     for (int q = threadIdx.x; q < nrows * g.mw; q += blockDim.x) mk[q] = 0u;
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ox = lane - g.r;
-    const bool xlane = lane < g.W;
+    const int ox = lane - r;
+    const bool xlane = lane < W;
+    const int par = ox & 1;
     unsigned long long cnt = 0;
     for (int rl = warp; rl < nrows; rl += blockDim.x >> 5) {
         const int ix = x0 + rl;
         const int64_t i = (int64_t)line * g.K + ix;
-        double xr[4][ASM_MAXJ];
+        double xr[NG][J];
 #pragma unroll
-        for (int gi = 0; gi < 4; ++gi)
+        for (int gi = 0; gi < NG; ++gi)
 #pragma unroll
-            for (int j = 0; j < ASM_MAXJ; ++j) {
-                const int t = (ox & 1) + 2 * j;
-                xr[gi][j] = (gi < NG && xlane && t < a.grp[gi].lens[0])
-                                ? blk(a, a.grp[gi].kind[0], t, ox, ix) : 0.0;
+            for (int j = 0; j < J; ++j) {
+                const int t = par + 2 * j;
+                xr[gi][j] = (xlane && t < a.grp[gi].lens[0]) ? blk(a, a.grp[gi].kind[0], t, ox, ix) : 0.0;
             }
         const bool xok = xlane && ix + ox >= 0 && ix + ox < g.K;
         uint32_t *mrow = mk + rl * g.mw;
-        double *vrow = vals + (size_t)i * g.S;
-        for (int sl = 0; sl < nsl; ++sl) {
-            const int oy = g.d > 1 ? sl % g.W - g.r : 0, oz = g.d > 2 ? sl / g.W - g.r : 0;
-            const bool ok = xok && (g.d < 2 || (iy + oy >= 0 && iy + oy < g.K)) &&
-                            (g.d < 3 || (iz + oz >= 0 && iz + oz < g.K));
-            const double *Hs = H + (size_t)sl * NG * TL;
-            double v = 0.0;
+        double *vrow = vals + (size_t)i * g.S + lane;
+        const double *Hs = H + par;
+        int sl = 0;
+        const int nz = g.d > 2 ? W : 1, ny = g.d > 1 ? W : 1;
+        for (int sz = 0; sz < nz; ++sz) {
+            const bool zok = g.d < 3 || (iz + sz - r >= 0 && iz + sz - r < g.K);
+            for (int sy = 0; sy < ny; ++sy, ++sl, Hs += NG * HT) {
+                const bool ok = xok && zok && (g.d < 2 || (iy + sy - r >= 0 && iy + sy - r < g.K));
+                double v = 0.0;
 #pragma unroll
-            for (int gi = 0; gi < 4; ++gi) {
-                if (gi >= NG) break;
-                const int L0 = a.grp[gi].lens[0];
+                for (int gi = 0; gi < NG; ++gi)
 #pragma unroll
-                for (int j = 0; j < ASM_MAXJ; ++j) {
-                    const int t = (ox & 1) + 2 * j;
-                    if (t < L0) v += Hs[gi * TL + t] * xr[gi][j];
+                    for (int j = 0; j < J; ++j) v += Hs[gi * HT + 2 * j] * xr[gi][j];
+                const bool in = ok && fabs(v) >= 1e-300;
+                if (xlane) vrow[sl * W] = in ? v : 0.0;
+                const unsigned bits = __ballot_sync(0xffffffffu, in);
+                if (lane == 0 && bits) {
+                    const int s0 = sl * W, w0 = s0 >> 5, sh = s0 & 31;
+                    mrow[w0] |= bits << sh;
+                    if (sh && (bits >> (32 - sh))) mrow[w0 + 1] |= bits >> (32 - sh);
                 }
-            }
-            const bool in = ok && fabs(v) >= 1e-300;
-            if (xlane) vrow[sl * g.W + lane] = in ? v : 0.0;
-            const unsigned bits = __ballot_sync(0xffffffffu, in);
-            if (lane == 0 && bits) {
-                const int s0 = sl * g.W, w0 = s0 >> 5, sh = s0 & 31;
-                mrow[w0] |= bits << sh;
-                if (sh && (bits >> (32 - sh))) mrow[w0 + 1] |= bits >> (32 - sh);
             }
         }
         __syncwarp();
@@ -234,6 +238,29 @@ box_assemble_kernel(const __grid_constant__ AsmArgs a, double *__restrict__ vals
     __syncthreads();
     uint32_t *mdst = mask + ((size_t)line * g.K + x0) * g.mw;
     for (int q = threadIdx.x; q < nrows * g.mw; q += blockDim.x) mdst[q] = mk[q];
+}
+
+template <int NG>
+const void *assemble_kernel_j(int J) {
+    switch (J) {
+        case 1: return reinterpret_cast<const void *>(box_assemble_kernel<NG, 1>);
+        case 2: return reinterpret_cast<const void *>(box_assemble_kernel<NG, 2>);
+        case 3: return reinterpret_cast<const void *>(box_assemble_kernel<NG, 3>);
+        case 4: return reinterpret_cast<const void *>(box_assemble_kernel<NG, 4>);
+        case 5: return reinterpret_cast<const void *>(box_assemble_kernel<NG, 5>);
+        case 6: return reinterpret_cast<const void *>(box_assemble_kernel<NG, 6>);
+        case 7: return reinterpret_cast<const void *>(box_assemble_kernel<NG, 7>);
+        default: return reinterpret_cast<const void *>(box_assemble_kernel<NG, 8>);
+    }
+}
+
+const void *assemble_kernel(int NG, int J) {
+    switch (NG) {
+        case 1: return assemble_kernel_j<1>(J);
+        case 2: return assemble_kernel_j<2>(J);
+        case 3: return assemble_kernel_j<3>(J);
+        default: return assemble_kernel_j<4>(J);
+    }
 }
 
 // full[i] = 1 when every slot of row i is in the pattern (interior rows of a
@@ -811,15 +838,19 @@ extern "C" int lp_box_assemble(int d, int K, int n_groups, const int *lens, cons
     if (e != cudaSuccess) return fail(cuda_fail(e, "counter init", __FILE__, __LINE__));
     const int wd = d > 1 ? b.W : 1;
     const unsigned slot_lines = (unsigned)(d > 2 ? wd * wd : wd);
-    const size_t asm_smem = (size_t)slot_lines * n_groups * (tmax + 1) * sizeof(double) +
+    unsigned long long *cnt1 = cnt + 1;
+    const int asm_j = (tmax + 2) / 2;   // parity-matched degrees per group
+    const size_t asm_smem = (size_t)slot_lines * n_groups * 2 * asm_j * sizeof(double) +
                             (size_t)ASM_RB * b.mask_words * sizeof(uint32_t);
     if ((rc = dalloc(&b.full, (size_t)b.n, "full-row flags"))) return fail(rc);
-    if (b.W <= 32 && tmax + 1 <= 2 * ASM_MAXJ && asm_smem <= 200 * 1024) {
-        e = cudaFuncSetAttribute(box_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)asm_smem);
-        if (e != cudaSuccess) return fail(cuda_fail(e, "assembly attribute", __FILE__, __LINE__));
-        box_assemble_kernel<<<dim3((unsigned)a.g.nlines, (unsigned)ceil_div(K, ASM_RB)), 256,
-                              asm_smem>>>(a, b.values, b.mask, b.full, cnt, cnt + 1);
+    const void *akern = assemble_kernel(n_groups, asm_j);
+    if (b.W <= 32 && asm_j <= ASM_MAXJ && asm_smem <= 200 * 1024 &&
+        resident_blocks(akern, 256, asm_smem) > 0) {
+        void *args[] = {(void *)&a, (void *)&b.values, (void *)&b.mask, (void *)&b.full,
+                        (void *)&cnt, (void *)&cnt1};
+        e = cudaLaunchKernel(akern, dim3((unsigned)a.g.nlines, (unsigned)ceil_div(K, ASM_RB)), dim3(256),
+                             args, asm_smem, 0);
+        if (e != cudaSuccess) return fail(cuda_fail(e, "assembly launch", __FILE__, __LINE__));
         count_launch(1);
     } else {
         // general reach / degree: raw products, symmetrisation, pattern (three passes)
