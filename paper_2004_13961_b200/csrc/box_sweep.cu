@@ -984,7 +984,7 @@ int launch_sweep(lp_ilu *m, const double *rhs, double *out, int *ticket, cudaStr
 int box_build_bands(lp_ilu *m, cudaStream_t st) {
     BoxLayout &b = m->box;
     Geom g = geom_of(b);
-    if (box_sweep3d_applies(g)) return LP_OK;   // the 3-D sweeps read the factors directly
+    if (box_sweep3d_applies(g)) return box_build_even(m, st);   // the 3-D sweeps read the factors directly
     const int bs = band_stride(g);
     int rc;
     if (!b.band_lo && ((rc = dalloc(&b.band_lo, (size_t)b.n * bs, "band")) ||

@@ -79,7 +79,8 @@ struct S3 {
 
 struct Sweep3Args {
     Geom g;
-    const double *lu;
+    const double *lu;            // factor rows, a.rows doubles apart
+    int64_t rows;                // row stride of lu (S for the box layout)
     const double *rhs;
     double *out;
     int *ticket;
@@ -396,7 +397,14 @@ __global__ void __launch_bounds__(S3<R>::NT, 1) box_sweep3d_kernel(const __grid_
 // group of up to LPB lines with the SAME wavefront key (independent of each other)
 // and advances them in lockstep: one TMA copy per line per step, producer lane
 // (line j, source q) in segments of NQP lanes, serial lane j runs line j.
-template <int R>
+// ST = 2: the even-offset pattern of T = 0 (all in-pattern offsets even in every
+// axis; 27 of the 125 slots at r = 2).  The factors are then compacted to the
+// even slots (EvenBox, a reach-1 box of stride 2: 27 values per row) and the
+// kernel runs with virtual reach R = 1: slot (a, b, c) is the real offset
+// (2a, 2b, 2c), the in-line recurrence steps back 2 rows, and the producers'
+// windows hold real x offsets -2R..2R.  Per row the sweeps stream 13 / 14
+// values instead of 62 / 63.
+template <int R, int ST = 1>
 struct S3m {
     static constexpr int W = 2 * R + 1, W2 = W * W, S = W2 * W, C = (S - 1) / 2;
     static constexpr int NQ = R * W + R;
@@ -407,14 +415,18 @@ struct S3m {
     static constexpr int NT = 32 * (NPW + 3);   // + loader, serial, watcher warps
     static constexpr int ROWD = (C + 1 + 1 + 1) / 2 * 2;
     static constexpr int NR = 6;
-    static constexpr int P = W;   // window look-ahead (divides W)
+    static constexpr int WR = 2 * R * ST + 1;   // producer window (real x offsets)
+    static constexpr int P = WR;                // window look-ahead (divides WR)
+    static constexpr int RR = R * ST;           // real reach
 };
 
-template <bool FWD, int R>
-__global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const __grid_constant__ Sweep3Args a) {
-    using G = S3m<R>;
-    constexpr int W = G::W, S = G::S, C = G::C, NQ = G::NQ, NQP = G::NQP, LPB = G::LPB;
+template <bool FWD, int R, int ST>
+__global__ void __launch_bounds__(S3m<R, ST>::NT, 1) box_sweep3d_multi_kernel(const __grid_constant__ Sweep3Args a) {
+    using G = S3m<R, ST>;
+    constexpr int W = G::W, C = G::C, NQ = G::NQ, NQP = G::NQP, LPB = G::LPB;
     constexpr int NPW = G::NPW, PPL = G::PPL, ROWD = G::ROWD, NR = G::NR, P3 = G::P;
+    constexpr int WR = G::WR, RR = G::RR;
+    const int64_t S = a.rows;
     extern __shared__ __align__(16) double ring[];          // [NR][LPB][ROWD], then rhs [LPB][K]
     __shared__ __align__(8) unsigned long long mbar[NR];
     __shared__ double red[RRED][LPB][PPL];
@@ -520,9 +532,9 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
             const int owner = owner_of(ly);
             double *const out = a.rep[owner];
             const int64_t row0 = (int64_t)L * K;
-            double h[R];
+            double h[RR];   // h[d-1] = output of the row d (real) steps back in processing order
 #pragma unroll
-            for (int d = 0; d < R; ++d) h[d] = 0.0;
+            for (int d = 0; d < RR; ++d) h[d] = 0.0;
             for (int u = 0; u < K; ++u) {
                 const long long gs = gstep + u;
                 const int slot = (int)(gs % NR);
@@ -535,10 +547,10 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
                     const int sh = (int)((i * S + base) & 1);
                     const unsigned rowa = ring_s + (unsigned)((slot * LPB + lane) * ROWD + sh) * 8;
 #pragma unroll
-                    for (int d = R; d >= 2; --d) {
-                        const bool ok = FWD ? x - d >= 0 : x + d < K;
+                    for (int d = R; d >= 2; --d) {   // virtual in-line slot d: real offset ST d
+                        const bool ok = FWD ? x - ST * d >= 0 : x + ST * d < K;
                         const double cf = lds(rowa + (unsigned)(FWD ? C - d : d) * 8);
-                        if (ok) acc = __fma_rn(-cf, h[d - 1], acc);
+                        if (ok) acc = __fma_rn(-cf, h[ST * d - 1], acc);
                     }
                     c1 = lds(rowa + (unsigned)(FWD ? C - 1 : 1) * 8);
                     if (!FWD) diag = lds(rowa);
@@ -557,14 +569,14 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
                         csum += v;
                     }
                     acc -= csum;
-                    if (FWD ? x >= 1 : x + 1 < K) acc = __fma_rn(-c1, h[0], acc);
+                    if (FWD ? x >= ST : x + ST < K) acc = __fma_rn(-c1, h[ST - 1], acc);
                     const double y = canon3(FWD ? acc : __ddiv_rn(acc, diag));
                     st_keep(out + i, y, pol_keep);
                     for (int v = 0; v < a.nranks; ++v)
-                        if (v != owner && ly >= a.ys[v] - R && ly < a.ys[v + 1] + R)
+                        if (v != owner && ly >= a.ys[v] - RR && ly < a.ys[v + 1] + RR)   // real reach
                             st_halo(a.rep[v] + i, y, a.sys != 0, pol_keep);
 #pragma unroll
-                    for (int d = R - 1; d >= 1; --d) h[d] = h[d - 1];
+                    for (int d = RR - 1; d >= 1; --d) h[d] = h[d - 1];
                     h[0] = y;
                 }
             }
@@ -573,7 +585,7 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
             const int p = tid - 96;
             const int j = p / NQP, q = p % NQP;
             const int ql = FWD ? q : NQ + 1 + q;
-            const int oy = ql % W - R, oz = ql / W - R;
+            const int oy = ST * (ql % W - R), oz = ST * (ql / W - R);   // real line offsets
             const int L = j < cnt ? line_of(j) : 0;
             const int ly = L % K, lz = L / K;
             const bool active = j < cnt && q < NQ && ly + oy >= 0 && ly + oy < K && lz + oz >= 0 && lz + oz < K;
@@ -583,21 +595,21 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
             auto fetch = [&](int pp) {
                 return (active && pp >= 0 && pp < K) ? ld_l2(srcp(pp), pol_keep) : 0.0;
             };
-            double win[W], yq[P3];   // loads P3 rows ahead; a sentinel is polled again when needed
+            double win[WR], yq[P3];   // loads P3 rows ahead; a sentinel is polled again when needed
 #pragma unroll
-            for (int k = 0; k < W; ++k) win[k] = 0.0;
+            for (int k = 0; k < WR; ++k) win[k] = 0.0;
 #pragma unroll
-            for (int pp = 0; pp < R; ++pp) win[pp % W] = fetch(pp);
+            for (int pp = 0; pp < RR; ++pp) win[pp % WR] = fetch(pp);
 #pragma unroll
-            for (int k = 0; k < P3; ++k) yq[k] = fetch(R + k);
+            for (int k = 0; k < P3; ++k) yq[k] = fetch(RR + k);
 #pragma unroll
-            for (int pp = 0; pp < R; ++pp)
-                if (active && pp < K) win[pp % W] = wait_value(srcp(pp), win[pp % W], a.sys != 0);
+            for (int pp = 0; pp < RR; ++pp)
+                if (active && pp < K) win[pp % WR] = wait_value(srcp(pp), win[pp % WR], a.sys != 0);
             const int coff = ql * W;
             const int64_t row0 = (int64_t)L * K;
-            for (int u0 = 0; u0 < K; u0 += W) {
+            for (int u0 = 0; u0 < K; u0 += WR) {
 #pragma unroll
-                for (int k = 0; k < W; ++k) {
+                for (int k = 0; k < WR; ++k) {
                     const int u = u0 + k;
                     if (u < K) {
                         const long long gs = gstep + u;
@@ -605,10 +617,10 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
                         const int x = FWD ? u : K - 1 - u;
                         const int64_t i = row0 + x;
                         {
-                            const int pp = u + R;
+                            const int pp = u + RR;
                             double v = yq[k % P3];
                             if (active && pp < K) v = wait_value(srcp(pp), v, a.sys != 0);
-                            win[(k + R) % W] = v;
+                            win[(k + RR) % WR] = v;
                             yq[k % P3] = fetch(pp + P3);
                         }
                         wait_row(slot, gs);
@@ -618,10 +630,10 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
                             const unsigned rowa = ring_s + (unsigned)((slot * LPB + j) * ROWD + sh + coff - base) * 8;
 #pragma unroll
                             for (int jj = 0; jj < W; ++jj) {
-                                const int d = FWD ? jj - R : R - jj;
+                                const int d = ST * (FWD ? jj - R : R - jj);   // real x offset
                                 const double lv = lds(rowa + (unsigned)jj * 8);
-                                if (jj & 1) s1 = __fma_rn(lv, win[((k + d) % W + W) % W], s1);
-                                else s0 = __fma_rn(lv, win[((k + d) % W + W) % W], s0);
+                                if (jj & 1) s1 = __fma_rn(lv, win[((k + d) % WR + WR) % WR], s1);
+                                else s0 = __fma_rn(lv, win[((k + d) % WR + WR) % WR], s0);
                             }
                         }
                         double sum = s0 + s1;
@@ -640,12 +652,12 @@ __global__ void __launch_bounds__(S3m<R>::NT, 1) box_sweep3d_multi_kernel(const 
     }
 }
 
-template <bool FWD, int R>
+template <bool FWD, int R, int ST = 1>
 int launch3m(const Sweep3Args &a, cudaStream_t st) {
-    using G = S3m<R>;
+    using G = S3m<R, ST>;
     const size_t smem = ((size_t)G::NR * G::LPB * G::ROWD + (size_t)G::LPB * a.g.K) * sizeof(double);
     LP_ARG(smem <= 227 * 1024, "3-D sweep needs %zu bytes of shared memory (K = %d)", smem, a.g.K);
-    auto kern = box_sweep3d_multi_kernel<FWD, R>;
+    auto kern = box_sweep3d_multi_kernel<FWD, R, ST>;
     const int nblocks = resident_blocks(reinterpret_cast<const void *>(kern), G::NT, smem);
     if (nblocks < 1) return LP_ERR_ARG;
     int blocks = nblocks < a.ngroups ? nblocks : a.ngroups;
@@ -687,6 +699,67 @@ int dispatch3(const Sweep3Args &a, int r, cudaStream_t st) {
 }
 
 }  // namespace
+
+namespace {
+// any in-pattern slot with an odd offset coordinate?  oddm[w]: odd-offset slots of word w
+__global__ void odd_slots_kernel(Geom g, const uint32_t *__restrict__ mask, const uint32_t *__restrict__ oddm,
+                                 int *any) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < g.n * g.mw;
+         q += (int64_t)gridDim.x * blockDim.x)
+        if (mask[q] & oddm[q % g.mw]) {
+            *any = 1;
+            return;
+        }
+}
+
+// even[i][e] = lu[i][slot of offset 2 (a, b, c)], (a, b, c) in {-1, 0, 1}^3, a fastest
+__global__ void even_compact_kernel(Geom g, const double *__restrict__ lu, double *__restrict__ even) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < g.n * 27;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = q / 27;
+        const int e = (int)(q - i * 27);
+        const int ax = e % 3 - 1, ay = (e / 3) % 3 - 1, az = e / 9 - 1;
+        const int s = (2 * ax + g.r) + g.W * ((2 * ay + g.r) + g.W * (2 * az + g.r));
+        even[q] = lu[i * g.S + s];
+    }
+}
+}  // namespace
+
+// T = 0 patterns (reach 2, every in-pattern offset even): compact the factors to
+// the 27 even slots for the sweeps (13 / 14 values per row instead of 62 / 63).
+// Skipped when the pattern has odd offsets or the copy does not fit.
+int box_build_even(lp_ilu *m, cudaStream_t st) {
+    BoxLayout &b = m->box;
+    Geom g = geom_of(b);
+    if (g.d != 3 || g.r != 2 || !b.mask) return LP_OK;
+    std::vector<uint32_t> oddm(g.mw, 0u);
+    for (int s = 0; s < g.S; ++s) {
+        const int ox = s % g.W - g.r, oy = (s / g.W) % g.W - g.r, oz = s / (g.W * g.W) - g.r;
+        if ((ox & 1) || (oy & 1) || (oz & 1)) oddm[s >> 5] |= 1u << (s & 31);
+    }
+    uint32_t *d_odd = nullptr;
+    int *d_any = nullptr;
+    int rc;
+    if ((rc = salloc(&d_odd, g.mw, "odd slots", st)) || (rc = salloc(&d_any, 1, "flag", st))) return rc;
+    LP_CUDA(cudaMemcpyAsync(d_odd, oddm.data(), g.mw * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    LP_CUDA(cudaMemsetAsync(d_any, 0, sizeof(int), st));
+    odd_slots_kernel<<<num_sms() * 8, 256, 0, st>>>(g, b.mask, d_odd, d_any);
+    count_launch();
+    int any = 1;
+    LP_CUDA(cudaMemcpyAsync(&any, d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
+    LP_CUDA(cudaStreamSynchronize(st));
+    sfree(d_odd, st);
+    sfree(d_any, st);
+    if (any) return LP_OK;
+    if (!b.even && dalloc(&b.even, (size_t)g.n * 27 + 2, "even-slot factors") != LP_OK) {
+        b.even = nullptr;   // no room: the sweeps stream the box rows
+        return LP_OK;
+    }
+    even_compact_kernel<<<num_sms() * 16, 256, 0, st>>>(g, b.lu, b.even);
+    count_launch();
+    LP_CHECK_LAUNCH();
+    return LP_OK;
+}
 
 bool box_sweep3d_applies(const Geom &g) {
     return g.d == 3 && g.r >= 2 && g.r <= 10 && g.K >= 1;
@@ -812,6 +885,7 @@ int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket
     Sweep3Args a;
     a.g = g;
     a.lu = m->box.lu;
+    a.rows = g.S;
     a.ticket = ticket;
     a.order = m->box.line_order;
     a.nrun = g.nlines;
@@ -867,6 +941,11 @@ int box_sweep3d(lp_ilu *m, bool fwd, const double *rhs, double *out, int *ticket
         g_trace_n = trn;
     }
 #endif
+    if (m->box.even && g.r == 2) {
+        a.lu = m->box.even;
+        a.rows = 27;
+        return fwd ? launch3m<true, 1, 2>(a, st) : launch3m<false, 1, 2>(a, st);
+    }
     return fwd ? dispatch3<true>(a, g.r, st) : dispatch3<false>(a, g.r, st);
 }
 

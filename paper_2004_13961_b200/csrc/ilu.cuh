@@ -36,6 +36,9 @@ struct BoxLayout {
         int *order = nullptr, *groups = nullptr;
         int norder = 0, ngroups = 0;
     } rank_order[2];
+    // even-offset pattern (T = 0: every in-pattern offset even in each axis): the
+    // factors compacted to the 27 even slots of the r = 2 box, [n][27] (3-D sweeps)
+    double *even = nullptr;
     // 2-D factorisation (ilu_box2d.cu): block tasks in key order, RN(1/u_ii) per row
     int *ilu_tasks = nullptr;
     int ilu_ntask = 0, ilu_nb = 0;
@@ -95,6 +98,7 @@ int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st);
 int box_spmv(lp_ilu *m, const double *x, double *y, cudaStream_t st);
 int box_export(const lp_ilu *m, int which, int64_t *indptr, int32_t *indices, double *values);
 int box_build_bands(lp_ilu *m, cudaStream_t st);
+int box_build_even(lp_ilu *m, cudaStream_t st);
 int box_apply(lp_ilu *m, const double *r, double *z, const SweepScratch &s, cudaStream_t st);
 int box_ilu0_2d_tasks(lp_ilu *m, const double *src, double tol, unsigned long long *key, int *done,
                       cudaStream_t st);

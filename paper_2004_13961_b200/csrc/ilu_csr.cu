@@ -281,7 +281,7 @@ extern "C" int lp_ilu_destroy(lp_ilu *m) {
     void *ptrs[] = {m->indptr, m->indices, m->values, m->lu, m->diag, m->flags, m->ticket,
                     m->bad, m->box.values, m->box.lu, m->box.mask,
                     m->box.band_lo, m->box.band_up, m->box.diag, m->box.line_order,
-                    m->box.line_groups, m->box.full, m->box.ilu_tasks, m->box.rdiag};
+                    m->box.line_groups, m->box.full, m->box.ilu_tasks, m->box.rdiag, m->box.even};
     for (void *p : ptrs)
         if (p) dfree(p);
     for (auto &ro : m->box.rank_order) {

@@ -369,6 +369,7 @@ def test_cuda_stages_match_oracle():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,N,T,G", [("cfg4", 24, 8, 2), ("cfg4", 24, 8, 3), ("cfg5", 20, 3, 4),
+                                        ("cfg5", 26, 0, 3), ("cfg5", 21, 0, 2),
                                         ("cfg4", 40, 8, 4), ("cfg5", 24, 0, 3), ("cfg5", 20, 2, 2)])
 def test_rank_sweeps_bit_identical(name, N, T, G):
     """Sweeps over G y-slab ranks with halo publication == the one-rank sweeps."""
@@ -450,7 +451,8 @@ def test_rank_pcg_one_rank_nccl_bit_identical(name, N, T):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,N,T", [("cfg5", 24, 0), ("cfg5", 20, 1), ("cfg4", 18, 2), ("cfg5", 16, 3),
+@pytest.mark.parametrize("name,N,T", [("cfg5", 24, 0), ("cfg5", 37, 0), ("cfg4", 22, 0),
+                                      ("cfg5", 20, 1), ("cfg4", 18, 2), ("cfg5", 16, 3),
                                       ("cfg4", 14, 8)])
 def test_box_sweeps_match_csr_sweeps(name, N, T):
     """The 3-D box sweeps (small-reach multi-line kernel for r <= 4, the line kernel
