@@ -156,6 +156,22 @@ int lp_box_assemble(int d, int K, int n_groups, const int *lens,
                     const int *stiff_axis, const double *const *hats,
                     int tmax, const double *blocks, lp_ilu **out);
 
+/* building_blocks_1d (precond.py:118-161) on the GPU: the diagonals of the
+ * exact-quadrature 1-D blocks for t = 0..T on the Q-point Gauss rule
+ * (nodes, weights: host or device, Q >= K + T/2 + 2), written to `blocks`
+ * (host or device) in the layout lp_box_assemble takes:
+ * blocks[kind][t][o + R][i], R = T + 2.  Same operation order as the
+ * reference (node order, chunks of 512 nodes): bit-identical diagonals. */
+int lp_blocks_1d(int T, int K, int Q, const double *nodes, const double *weights,
+                 double *blocks);
+
+/* _mass_contract (operator.py:131-143) on every axis of a P^d Legendre
+ * coefficient tensor: out_k = 2 v_k/(2k+1) - 2 v_{k+2}/(2k+5), P^d -> K^d,
+ * K = P - 2 (the last step of assemble_rhs, operator.py:213-222).  in/out
+ * are device vectors, x fastest; axis 0 first, each operation separately
+ * rounded (bit-identical to the reference's numpy expression). */
+int lp_mass_contract(int d, int P, const double *in, double *out, void *stream);
+
 /* Number of stored entries (SparseMatrix.nnz) and CSR export (host arrays
  * sized by nnz; indices/values may be NULL to fetch only indptr). */
 int lp_matrix_nnz(const lp_ilu *m, int64_t *nnz);

@@ -54,6 +54,8 @@ _SIGS = {
     "lp_csr_create": (_i32, [_i64, _i64, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
     "lp_box_assemble": (_i32, [_i32, _i32, _i32, _vp, _vp, ctypes.POINTER(_vp), _i32, _vp,
                                ctypes.POINTER(_vp)]),
+    "lp_blocks_1d": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp]),
+    "lp_mass_contract": (_i32, [_i32, _i32, _vp, _vp, _vp]),
     "lp_matrix_nnz": (_i32, [_vp, ctypes.POINTER(_i64)]),
     "lp_matrix_export": (_i32, [_vp, _i32, _vp, _vp, _vp]),
     "lp_ilu0": (_i32, [_vp, _dbl, ctypes.POINTER(_i64), _vp]),

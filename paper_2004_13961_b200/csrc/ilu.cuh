@@ -103,6 +103,7 @@ int box_apply(lp_ilu *m, const double *r, double *z, const SweepScratch &s, cuda
 int box_ilu0_2d_tasks(lp_ilu *m, const double *src, double tol, unsigned long long *key, int *done,
                       cudaStream_t st);
 int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_t st);
+int box_ilu0_3d_blocks(lp_ilu *m, double tol, unsigned long long *key, cudaStream_t st);
 struct Geom;
 bool box_sweep3d_applies(const Geom &g);
 int ensure_line_order(BoxLayout &b, cudaStream_t st);

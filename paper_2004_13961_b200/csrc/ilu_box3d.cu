@@ -40,10 +40,16 @@
 #define LP_ILU3_LEVEL_MAX_R 8   // level order for reach <= this; natural order above (measured, barrier-free kernel: r=2 11x faster, r=4 1.3x, r=7 1.24x, r=10 1.19x slower)
 #endif
 
+#ifndef LP_ILU3_BLK_MIN_R
+#define LP_ILU3_BLK_MIN_R 9     // row-block kernel from this reach on
+#endif
+
 namespace lp {
 
-extern unsigned long long *g_ilu_trace;
-extern size_t g_ilu_trace_n;
+#ifdef LP_ILU_TRACE
+unsigned long long *g_ilu_trace = nullptr;   // dev builds: row timestamps of the last factorisation
+size_t g_ilu_trace_n = 0;
+#endif
 
 namespace {
 
@@ -413,6 +419,8 @@ int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_
     BoxLayout &b = m->box;
     Geom g = geom_of(b);
     if (g.d != 3) return LP_ERR_ARG;
+    // large reach: blocks of x-adjacent rows share their pivot rows (ilu_box3d_blk.cu)
+    if (g.r >= LP_ILU3_BLK_MIN_R && box_ilu0_3d_blocks(m, tol, key, st) == LP_OK) return LP_OK;
     Ilu3Args a;
     a.g = g;
     a.lu = b.lu;

@@ -244,13 +244,28 @@ def mass_contract(v, axis):
     return np.moveaxis(out, -1, axis)
 
 
+def mass_contract_device(fhat_flat, dim, P):
+    """All-axes mass contraction of a device P^d Legendre coefficient vector
+    (x fastest) on the GPU: K^d device vector (``lp_mass_contract``)."""
+    out = device.empty((P - 2) ** dim)
+    _lib.check(_lib.load().lp_mass_contract(dim, P, fhat_flat.data_ptr(), out.data_ptr(),
+                                            _lib.stream_ptr()), "mass contraction")
+    return out
+
+
 def assemble_rhs(spec, plan):
     """Load vector F_k = (I_N f, phi_k) (operator.py:213-222): GPU FDLT of the
-    sampled f, then the closed-form mass contraction per axis."""
+    sampled f, then the closed-form mass contraction per axis, also on the GPU
+    (bit-identical to the reference's numpy expression)."""
     spec._check_plan(plan)
     if spec.rhs is None:
         raise ValueError("problem spec has no right-hand-side field")
-    fh = tensor_fdlt(plan, spec.grid_values(plan, "rhs"))
-    for a in range(spec.dim):
-        fh = mass_contract(fh, a)
-    return SpectralCoeffs(fh)
+    d, P = spec.dim, plan.order
+    vals = device.to_device(device.fortran_flat(np.broadcast_to(
+        spec.grid_values(plan, "rhs"), (P,) * d)))
+    fh = device.empty(P ** d)
+    lib = _lib.load()
+    _lib.check(lib.lp_tensor_fdlt(plan.handle, d, vals.data_ptr(), fh.data_ptr(), _lib.stream_ptr()),
+               "assemble_rhs")
+    out = mass_contract_device(fh, d, P)
+    return SpectralCoeffs(device.from_fortran_flat(device.host(out), spec.n_modes, d))

@@ -1,10 +1,11 @@
 """Truncated-coefficient preconditioner M (drop-in for precond.py:26-318).
 
-Host setup (restating the reference, tiny): ``expand_coefficient`` truncates
-each coefficient to a degree-t Legendre series on a 32-point grid, and
-``building_blocks_1d`` forms the diagonals of the exact-quadrature 1-D blocks
-S^(t), M^(t).  The K^d-sized work -- the hat-weighted sum of Kronecker
-products, the symmetrisation and the pattern/compression -- runs on the GPU
+``expand_coefficient`` truncates each coefficient to a degree-t Legendre series
+on a 32-point grid (host: the fields are Python callables, 32^d samples).
+``building_blocks_1d`` -- the diagonals of the exact-quadrature 1-D blocks
+S^(t), M^(t) -- runs on the GPU (``lp_blocks_1d``), and so does the K^d-sized
+work: the hat-weighted sum of Kronecker products, the symmetrisation and the
+pattern/compression
 (``lp_box_assemble``) straight into the implicit-offset layout the ILU(0)
 kernels consume; no CSR is built unless the caller asks for it.
 """
@@ -22,9 +23,6 @@ from .sparse import SparseMatrix
 
 __all__ = ["TruncatedCoefficient", "BandedBlock", "expand_coefficient",
            "building_blocks_1d", "assemble_M", "predicted_bandwidth"]
-
-_CHUNK = 512
-
 
 @dataclass(frozen=True)
 class TruncatedCoefficient:
@@ -93,10 +91,30 @@ def _offsets(kind, t):
 _BLOCKS = {}
 
 
+def _block_stack(T, K, rule):
+    """blocks[kind][t][o + R][i] = entry (i, i+o) of S^(t) (kind 0) / M^(t)
+    (kind 1), R = T + 2: the exact-quadrature diagonals, computed on the GPU
+    (``lp_blocks_1d``) in the reference's operation order (precond.py:118-161:
+    nodes in order, a partial sum per chunk of 512 nodes), so they are
+    bit-identical to the reference's.  Memoised per (T, K, rule)."""
+    key = (int(T), int(K), rule.nodes.tobytes(), rule.weights.tobytes())
+    hit = _BLOCKS.get(key)
+    if hit is None:
+        R = T + 2
+        hit = np.zeros((2, T + 1, 2 * R + 1, K))
+        nodes = np.ascontiguousarray(rule.nodes, dtype=float)
+        weights = np.ascontiguousarray(rule.weights, dtype=float)
+        _lib.check(_lib.load().lp_blocks_1d(int(T), int(K), int(rule.order), nodes.ctypes.data,
+                                            weights.ctypes.data, hit.ctypes.data), "building_blocks_1d")
+        hit.flags.writeable = False
+        _BLOCKS[key] = hit
+    return hit
+
+
 def building_blocks_1d(T, K, plan):
     """Exact-quadrature diagonals of S^(t) = (L_t phi', phi') and
-    M^(t) = (L_t phi, phi), t = 0..T (precond.py:118-161).  Memoised per
-    (T, K, rule); the diagonals are read-only."""
+    M^(t) = (L_t phi, phi), t = 0..T (precond.py:118-161), as read-only
+    ``BandedBlock`` views of the GPU-built stack."""
     if T < 0 or K < 1:
         raise ValueError("need T >= 0 and K >= 1")
     rule = plan if isinstance(plan, GaussRule) else plan.rule
@@ -104,41 +122,13 @@ def building_blocks_1d(T, K, plan):
     if rule.order < needed:
         raise ValueError(f"quadrature order {rule.order} is insufficient for exact "
                          f"blocks with T={T}, K={K}: need at least {needed}")
-    key = (int(T), int(K), rule.nodes.tobytes(), rule.weights.tobytes())
-    hit = _BLOCKS.get(key)
-    if hit is None:
-        hit = _building_blocks_1d(int(T), int(K), rule)
-        for bl in hit:
-            for b in bl:
-                for dg in b.diags.values():
-                    dg.flags.writeable = False
-        _BLOCKS[key] = hit
-    return hit
-
-
-def _building_blocks_1d(T, K, rule):
-    acc = {kind: [{o: np.zeros(K) for o in _offsets(kind, t)} for t in range(T + 1)]
-           for kind in ("stiff", "mass")}
-    dcoef = -(2.0 * np.arange(K) + 3.0)
-    for lo in range(0, rule.order, _CHUNK):
-        hi = min(lo + _CHUNK, rule.order)
-        tab = legendre_table(rule.nodes[lo:hi], K + 1)
-        basis = {"stiff": dcoef * tab[:, 1:K + 1], "mass": tab[:, :K] - tab[:, 2:K + 2]}
-        w = rule.weights[lo:hi]
-        for t in range(T + 1):
-            wt = w * tab[:, t]
-            for kind in ("stiff", "mass"):
-                b = basis[kind]
-                for o, dg in acc[kind][t].items():
-                    if o >= 0:
-                        dg[:K - o] += np.einsum("p,pi,pi->i", wt, b[:, :K - o], b[:, o:])
-    for kind in ("stiff", "mass"):
-        for t in range(T + 1):
-            for o, dg in acc[kind][t].items():
-                if o < 0:
-                    dg[-o:] = acc[kind][t][-o][:K + o]
-    return ([BandedBlock("stiff", t, K, acc["stiff"][t]) for t in range(T + 1)],
-            [BandedBlock("mass", t, K, acc["mass"][t]) for t in range(T + 1)])
+    stack = _block_stack(int(T), int(K), rule)
+    R = T + 2
+    out = []
+    for kind, name in enumerate(("stiff", "mass")):
+        out.append([BandedBlock(name, t, K, {o: stack[kind, t, o + R] for o in _offsets(name, t)})
+                    for t in range(T + 1)])
+    return out[0], out[1]
 
 
 def _groups(spec, t1, t2):
@@ -181,13 +171,7 @@ def assemble_M(spec, t1, t2, plan=None):
     groups = _groups(spec, t1, t2)
     tmax = max(h.shape[a] for h, _ in groups for a in range(d)) - 1
     rule = gauss_rule(K + tmax // 2 + 2)
-    s_blocks, m_blocks = building_blocks_1d(tmax, K, rule)
-    R = tmax + 2
-    blocks = np.zeros((2, tmax + 1, 2 * R + 1, K))
-    for kind, bl in enumerate((s_blocks, m_blocks)):
-        for t, b in enumerate(bl):
-            for o, dg in b.diags.items():
-                blocks[kind, t, o + R] = dg
+    blocks = _block_stack(tmax, K, rule)
     lens = np.array([h.shape for h, _ in groups], dtype=np.int32).reshape(-1)
     stiff = np.array([-1 if s is None else s for _, s in groups], dtype=np.int32)
     hats = [np.ascontiguousarray(h, dtype=float) for h, _ in groups]

@@ -252,7 +252,7 @@ def test_ilu0_csr_bitwise_3d(golden, name, N, T):
                                       ("cfg5", 20, 2), ("cfg4", 9, 1), ("cfg2", 20, 10),
                                       ("cfg2", 520, 4), ("cfg3", 64, 12), ("cfg3", 150, 12),
                                       ("cfg2", 100, 10), ("cfg2", 37, 0), ("cfg2", 45, 1),
-                                      ("cfg3", 40, 13)])
+                                      ("cfg3", 40, 13), ("cfg4", 24, 8), ("cfg5", 25, 7)])
 def test_box_factors_bitwise_vs_csr(name, N, T):
     """The box-layout factorisation (3-D: row-per-CTA kernel; 2-D: task graph)
     equals, bit for bit, the CSR kernel on the same M -- which reproduces the
@@ -374,3 +374,45 @@ def test_pcg_indefinite_and_kmax():
     _, rep = pcg_solve(spec, SolverConfig(epsilon=1e-14, k_max=2), TransformPlan(17),
                        SpectralCoeffs(np.ones((15, 15))))
     assert not rep.converged and rep.iterations == 2
+
+
+# ---------------------------------------------------------------- front end on the GPU
+@pytest.mark.parametrize("K,T", [(40, 6), (127, 8), (255, 10), (700, 12), (9, 4)])
+def test_building_blocks_bitwise_vs_oracle(K, T):
+    """lp_blocks_1d (precond.py:118-161 on the GPU): the diagonals of S^(t), M^(t)
+    equal the CPU restatement bit for bit (same operation order; K = 700 spans
+    two 512-node chunks)."""
+    from paper_2004_13961_b200 import precond, quadrature
+    rule = quadrature.gauss_rule(K + T // 2 + 2)
+    S, M = precond.building_blocks_1d(T, K, rule)
+    So, Mo = orc.building_blocks_1d(T, K, rule.nodes, rule.weights)
+    for t in range(T + 1):
+        assert set(S[t].diags) == set(So[t]) and set(M[t].diags) == set(Mo[t])
+        for o in S[t].diags:
+            np.testing.assert_array_equal(S[t].diags[o], So[t][o])
+        for o in M[t].diags:
+            np.testing.assert_array_equal(M[t].diags[o], Mo[t][o])
+
+
+@pytest.mark.parametrize("d,P", [(1, 129), (2, 67), (3, 21), (3, 3), (2, 257)])
+def test_mass_contract_bitwise(d, P):
+    """lp_mass_contract equals the reference's numpy expression
+    (operator.py:131-143, axis 0 first) bit for bit."""
+    from paper_2004_13961_b200 import device
+    from paper_2004_13961_b200.operator import mass_contract_device
+    fh = np.random.default_rng(P).standard_normal((P,) * d)
+    ref = wl.mass_contract_series(fh)
+    out = device.host(mass_contract_device(device.to_device(fh.flatten(order="F")), d, P))
+    np.testing.assert_array_equal(out.reshape((P - 2,) * d, order="F"), ref)
+
+
+def test_assemble_rhs_matches_oracle():
+    """assemble_rhs (operator.py:213-222): GPU FDLT + GPU contraction."""
+    from paper_2004_13961_b200 import assemble_rhs, coefficients
+    w = wl.cfg2(N=48)
+    f = coefficients.CoefficientField(2, lambda x, y: np.exp(x) * np.cos(2 * y) + x * y, "f")
+    spec = ProblemSpec(dim=2, N=w.N, beta=w.beta, alpha=w.alpha, rhs=f)
+    got = assemble_rhs(spec, TransformPlan(w.N + 1)).data
+    ospec = ProblemSpec(dim=2, N=w.N, beta=w.beta, alpha=w.alpha, rhs=f)
+    ref = orc.assemble_rhs(ospec, orc.Plan(w.N + 1))
+    assert relerr(got, ref) < 1e-13

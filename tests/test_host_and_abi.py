@@ -67,18 +67,6 @@ def test_expand_coefficient_bitwise_vs_oracle(name, t):
     np.testing.assert_array_equal(a, b)
 
 
-def test_building_blocks_bitwise_vs_oracle():
-    K, T = 40, 6
-    rule = quadrature.gauss_rule(K + T // 2 + 2)
-    S, M = precond.building_blocks_1d(T, K, rule)
-    So, Mo = orc.building_blocks_1d(T, K, rule.nodes, rule.weights)
-    for t in range(T + 1):
-        for o in S[t].diags:
-            np.testing.assert_array_equal(S[t].diags[o], So[t][o])
-        for o in M[t].diags:
-            np.testing.assert_array_equal(M[t].diags[o], Mo[t][o])
-
-
 def test_building_blocks_insufficient_quadrature():
     with pytest.raises(ValueError, match="quadrature order"):
         precond.building_blocks_1d(4, 20, quadrature.gauss_rule(12))
