@@ -69,6 +69,16 @@ def mass_contract_series(fhat):
     return h
 
 
+def rhs_on_device(fhat):
+    """The same load vector built on the GPU: the P^d series coefficients are
+    uploaded once and contracted there (``lp_mass_contract``, bit-identical to
+    ``mass_contract_series``); returns the x-fastest device vector of K^d."""
+    from . import device
+    from .operator import mass_contract_device
+    h = np.asarray(fhat, dtype=float)
+    return mass_contract_device(device.to_device(h.flatten(order="F")), h.ndim, h.shape[0])
+
+
 def seeded_fhat(dim, P, seed=SEED_RHS):
     g = np.random.default_rng(seed).standard_normal((P,) * dim)
     scale = np.ones(())

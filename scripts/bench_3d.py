@@ -59,8 +59,7 @@ def run(w, loops, cpu_reps):
     spec = ProblemSpec(dim=w.dim, N=w.N, beta=w.beta, alpha=w.alpha)
     plan = TransformPlan(w.N + 1)
     cfg = SolverConfig(epsilon=w.rtol, preconditioner=(w.T, w.T))
-    F = wl.mass_contract_series(w.fhat)
-    fd = device.to_device(F.flatten(order="F"))
+    fd = wl.rhs_on_device(w.fhat)   # GPU mass contraction of the seeded series
     spec.device_operator(plan)
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]

@@ -34,8 +34,7 @@ spec = ProblemSpec(dim=w.dim, N=w.N, beta=w.beta, alpha=w.alpha)
 plan = TransformPlan(w.N + 1)
 cfg = SolverConfig(epsilon=w.rtol, preconditioner=(w.T, w.T))
 t0 = time.perf_counter()
-F = wl.mass_contract_series(w.fhat)
-fd = device.to_device(F.flatten(order="F"))
+fd = wl.rhs_on_device(w.fhat)   # GPU mass contraction of the seeded series
 spec.device_operator(plan)
 torch.cuda.synchronize()
 t1 = time.perf_counter()
