@@ -187,6 +187,12 @@ int lp_ilu0(lp_ilu *m, double pivot_tol, int64_t *bad_row, void *stream);
 int lp_forward_sub(lp_ilu *f, const double *r, double *y, void *stream);
 int lp_backward_sub(lp_ilu *f, const double *y, double *z, void *stream);
 int lp_precond_apply(lp_ilu *f, const double *r, double *z, void *stream);
+/* precond_apply with the PCG scalar rho = r'z (pcg.py:147-151) as a second
+ * output: rz points to two device doubles (a double-double pair, hi then lo).
+ * The 1-D / 2-D line-wavefront sweeps accumulate r'z inside the backward sweep
+ * (a part per x-line, summed in double-double in a fixed order: deterministic);
+ * the other sweep kernels follow with a deterministic dot on the same stream. */
+int lp_precond_apply_rz(lp_ilu *f, const double *r, double *z, double *rz, void *stream);
 /* y = M x with the ORIGINAL matrix (spmv, sparse.py:97-113). */
 int lp_spmv(lp_ilu *m, const double *x, double *y, void *stream);
 int lp_ilu_destroy(lp_ilu *m);

@@ -62,6 +62,7 @@ _SIGS = {
     "lp_forward_sub": (_i32, [_vp, _vp, _vp, _vp]),
     "lp_backward_sub": (_i32, [_vp, _vp, _vp, _vp]),
     "lp_precond_apply": (_i32, [_vp, _vp, _vp, _vp]),
+    "lp_precond_apply_rz": (_i32, [_vp, _vp, _vp, _vp, _vp]),
     "lp_spmv": (_i32, [_vp, _vp, _vp, _vp]),
     "lp_ilu_destroy": (_i32, [_vp]),
     "lp_pcg_solve": (_i32, [_vp, _vp, _vp, _vp, _i32, _dbl, _i64, _vp,

@@ -35,6 +35,7 @@
 #include "box_geom.cuh"
 #include "ilu.cuh"
 #include "smem_tma.cuh"
+#include "vector_ops.cuh"
 
 namespace lp {
 
@@ -116,6 +117,11 @@ struct SweepArgs {
     int csize;            // cluster size: lines of a batch (consecutive in sweep order)
     unsigned yr_ofs;      // byte offset of the line-handoff buffer [K] in dynamic smem
     unsigned long long *trace;   // LP_SWEEP_TRACE builds: per-line timestamps
+    // fused dot product (pcg.py:151, r'z inside the backward sweep): the serial
+    // warp of line L accumulates sum_x dotv[row] * out[row] and stores it to
+    // dotpart[L]; null = no dot
+    const double *dotv;
+    double *dotpart;
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -272,6 +278,11 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                 wcyc += clock64() - w0;
 #endif
             };
+            // fused dot: lane k holds dotv of row 32c + k of the current chunk (the
+            // next chunk's values are loaded a chunk ahead, off the chain)
+            const bool dot = a.dotv != nullptr;
+            double racc = 0.0, rv = 0.0, rvn = 0.0;
+            if (dot && lane < K) rvn = __ldg(a.dotv + row0 + ix_of(lane));
             stage(0);
             stage(1);
             stage(2);
@@ -302,7 +313,7 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
 #endif
             // HP: the line has a previous line (A_t from the group); a compile-time
             // flag so the step carries no branch on it
-            auto step = [&](const int t, auto HP) {
+            auto step = [&](const int t, auto HP, auto DT) {
                 constexpr bool hp = decltype(HP)::value;
                 const double q = qn, e1c = e1n, rd = rdn, spt = spn;
                 double c = cn, av = dn;
@@ -335,6 +346,7 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                 // broadcast before the update, off the y_t -> y_{t+1} chain
                 spn = __shfl_sync(0xffffffff, sp, (t + 1) & 31);
                 sp = ((unsigned)lane == ((unsigned)t & 31)) ? 0.0 : fma(q, y, sp);
+                if (decltype(DT)::value) racc = ((unsigned)lane == ((unsigned)t & 31)) ? fma(rv, y, racc) : racc;
                 e1 = e1c;
                 yprev = y;
             };
@@ -358,16 +370,31 @@ box_sweep_kernel(const __grid_constant__ SweepArgs a) {
                     for (int t = 32 * c; t < t1; ++t) {
                         if (t == th) mark(2);
                         if (t == th2 && lane == 0 && a.trace) a.trace[(size_t)tl * 16 + 15] = gtime();
-                        if (has_prev) step(t, std::true_type{});
-                        else step(t, std::false_type{});
+                        if (has_prev) step(t, std::true_type{}, std::false_type{});
+                        else step(t, std::false_type{}, std::false_type{});
                     }
                     continue;
                 }
 #endif
-                if (has_prev)
-                    for (int t = 32 * c; t < t1; ++t) step(t, std::true_type{});
-                else
-                    for (int t = 32 * c; t < t1; ++t) step(t, std::false_type{});
+                if (dot) {
+                    rv = rvn;
+                    const int tn = 32 * c + 32 + lane;
+                    rvn = tn < Kr ? __ldg(a.dotv + row0 + ix_of(tn)) : 0.0;
+                    if (has_prev)
+                        for (int t = 32 * c; t < t1; ++t) step(t, std::true_type{}, std::true_type{});
+                    else
+                        for (int t = 32 * c; t < t1; ++t) step(t, std::false_type{}, std::true_type{});
+                } else if (has_prev) {
+                    for (int t = 32 * c; t < t1; ++t) step(t, std::true_type{}, std::false_type{});
+                } else {
+                    for (int t = 32 * c; t < t1; ++t) step(t, std::false_type{}, std::false_type{});
+                }
+            }
+            if (dot) {
+                // the line's sum in a fixed order (xor butterfly over the lanes)
+#pragma unroll
+                for (int o = 16; o; o >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, o);
+                if (lane == 0) a.dotpart[L] = racc;
             }
 #ifdef LP_SWEEP_TRACE
             mark(3);
@@ -923,7 +950,8 @@ int launch_nq(const SweepArgs &a, const Geom &g, size_t smem, cudaStream_t st) {
 }
 
 template <bool FWD>
-int launch_sweep(lp_ilu *m, const double *rhs, double *out, int *ticket, cudaStream_t st) {
+int launch_sweep(lp_ilu *m, const double *rhs, double *out, int *ticket, cudaStream_t st,
+                 const double *dotv = nullptr, double *dotpart = nullptr) {
     Geom g = geom_of(m->box);
     if (box_sweep3d_applies(g)) {
         LP_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
@@ -945,6 +973,8 @@ int launch_sweep(lp_ilu *m, const double *rhs, double *out, int *ticket, cudaStr
     a.lo = FWD ? 0 : g.c + excl + 1;
     a.nslot = FWD ? g.c - excl : g.S - (g.c + excl + 1);
     a.trace = nullptr;
+    a.dotv = dotv;
+    a.dotpart = dotpart;
 #ifdef LP_SWEEP_TRACE
     {
         static unsigned long long *tr = nullptr;
@@ -1012,6 +1042,21 @@ int box_apply(lp_ilu *m, const double *r, double *z, const SweepScratch &s, cuda
     int rc = prefill(m->n, s.ytmp, z, st);
     if (!rc) rc = launch_sweep<true>(m, r, s.ytmp, s.tickets, st);
     if (!rc) rc = launch_sweep<false>(m, s.ytmp, z, s.tickets + 1, st);
+    return rc;
+}
+
+// The line-wavefront kernel can carry r'z in its backward sweep (1-D, 2-D and
+// the 3-D boxes it serves); the bandwidth-first 3-D sweeps cannot.
+bool box_apply_dot_fused(const lp_ilu *m) { return !box_sweep3d_applies(geom_of(m->box)); }
+
+// precond_apply with rz = r'z fused into the backward sweep: every line's
+// serial warp accumulates its part, the parts are summed in double-double in a
+// fixed order (sum_lines_dd).  rz: device dd pair.
+int box_apply_dot(lp_ilu *m, const double *r, double *z, const SweepScratch &s, double *rz, cudaStream_t st) {
+    int rc = prefill(m->n, s.ytmp, z, st);
+    if (!rc) rc = launch_sweep<true>(m, r, s.ytmp, s.tickets, st);
+    if (!rc) rc = launch_sweep<false>(m, s.ytmp, z, s.tickets + 1, st, r, s.dotpart);
+    if (!rc) rc = sum_lines_dd(s.dotpart, geom_of(m->box).nlines, rz, st);
     return rc;
 }
 

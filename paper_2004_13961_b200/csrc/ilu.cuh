@@ -75,6 +75,7 @@ struct SweepScratch {
     double *ytmp = nullptr;   // [n] forward-sweep result of precond_apply
     int *tickets = nullptr;   // [2] line / row tickets (forward, backward)
     int *flags = nullptr;     // [n] CSR sweeps: per-row progress
+    double *dotpart = nullptr;   // fused r'z: per-line parts (box) / dd block partials (others)
 };
 int scratch_alloc(const lp_ilu *m, SweepScratch &s, cudaStream_t st);
 void scratch_free(SweepScratch &s, cudaStream_t st);
@@ -90,6 +91,11 @@ struct RankLayout {
     double *peers[8] = {nullptr};
 };
 int ilu_apply(lp_ilu *m, const double *r, double *z, const SweepScratch &s, cudaStream_t st);
+// z = M^-1 r and rz = r'z (device double-double pair): fused into the backward
+// sweep where the kernel supports it, a deterministic dot on the same stream otherwise
+int ilu_apply_dot(lp_ilu *m, const double *r, double *z, const SweepScratch &s, double *rz, cudaStream_t st);
+bool box_apply_dot_fused(const lp_ilu *m);
+int box_apply_dot(lp_ilu *m, const double *r, double *z, const SweepScratch &s, double *rz, cudaStream_t st);
 int ilu_forward(lp_ilu *m, const double *r, double *y, const SweepScratch &s, cudaStream_t st);
 int ilu_backward(lp_ilu *m, const double *y, double *z, const SweepScratch &s, cudaStream_t st);
 int box_forward(lp_ilu *m, const double *r, double *y, int *ticket, cudaStream_t st);

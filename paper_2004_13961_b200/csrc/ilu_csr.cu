@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "ilu.cuh"
+#include "vector_ops.cuh"
 
 namespace lp {
 namespace {
@@ -206,13 +207,17 @@ int scratch_alloc(const lp_ilu *m, SweepScratch &s, cudaStream_t st) {
         (rc = salloc(&s.tickets, 2, "sweep tickets", st)))
         return rc;
     if (m->kind != MAT_BOX && (rc = salloc(&s.flags, (size_t)m->n, "sweep flags", st))) return rc;
-    return LP_OK;
+    // fused r'z: one part per x-line (box sweeps) or the dd block partials of dot_dd
+    size_t nd = 2 * RED_BLOCKS;
+    if (m->kind == MAT_BOX && (size_t)(m->n / m->box.K) > nd) nd = (size_t)(m->n / m->box.K);
+    return salloc(&s.dotpart, nd, "dot partials", st);
 }
 
 void scratch_free(SweepScratch &s, cudaStream_t st) {
     sfree(s.ytmp, st);
     sfree(s.tickets, st);
     sfree(s.flags, st);
+    sfree(s.dotpart, st);
     s = SweepScratch{};
 }
 
@@ -221,6 +226,12 @@ int ilu_apply(lp_ilu *m, const double *r, double *z, const SweepScratch &s, cuda
     if (m->kind == MAT_BOX) return box_apply(m, r, z, s, st);
     if ((rc = csr_fwd(m, r, s.ytmp, s.flags, s.tickets, st))) return rc;
     return csr_bwd(m, s.ytmp, z, s.flags, s.tickets + 1, st);
+}
+
+int ilu_apply_dot(lp_ilu *m, const double *r, double *z, const SweepScratch &s, double *rz, cudaStream_t st) {
+    if (m->kind == MAT_BOX && box_apply_dot_fused(m)) return box_apply_dot(m, r, z, s, rz, st);
+    const int rc = ilu_apply(m, r, z, s, st);
+    return rc ? rc : dot_dd(m->n, r, z, s.dotpart, rz, st);
 }
 
 int ilu_forward(lp_ilu *m, const double *r, double *y, const SweepScratch &s, cudaStream_t st) {
@@ -365,6 +376,13 @@ extern "C" int lp_precond_apply(lp_ilu *m, const double *r, double *z, void *str
     LP_ARG(m->factored, "matrix has not been factored (call lp_ilu0)");
     cudaStream_t st = as_stream(stream);
     return with_scratch(m, st, [&](const SweepScratch &s) { return ilu_apply(m, r, z, s, st); });
+}
+
+extern "C" int lp_precond_apply_rz(lp_ilu *m, const double *r, double *z, double *rz, void *stream) {
+    LP_ARG(m->factored, "matrix has not been factored (call lp_ilu0)");
+    LP_ARG(rz != nullptr, "rz must point to two device doubles");
+    cudaStream_t st = as_stream(stream);
+    return with_scratch(m, st, [&](const SweepScratch &s) { return ilu_apply_dot(m, r, z, s, rz, st); });
 }
 
 extern "C" int lp_spmv(lp_ilu *m, const double *x, double *y, void *stream) {

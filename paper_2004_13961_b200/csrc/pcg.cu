@@ -91,13 +91,15 @@ int iteration(const Loop &L, int64_t it, cudaStream_t st) {
     double *sc = ws.scal;
     int rc;
     const double *zz = ws.r;
-    if (L.pre) {
-        if ((rc = ilu_apply(L.pre, ws.r, ws.z, ws.sweep, st))) return rc;
-        zz = ws.z;
-    }
     double *rho_new = sc + ((it & 1) ? S_RHO1 : S_RHO0);
     double *rho_old = sc + ((it & 1) ? S_RHO0 : S_RHO1);
-    if ((rc = dot_dd(L.n, ws.r, zz, ws.partial, rho_new, st))) return rc;
+    if (L.pre) {
+        // z = M^-1 r with rho = r'z carried by the backward sweep (pcg.py:147-151)
+        if ((rc = ilu_apply_dot(L.pre, ws.r, ws.z, ws.sweep, rho_new, st))) return rc;
+        zz = ws.z;
+    } else if ((rc = dot_dd(L.n, ws.r, zz, ws.partial, rho_new, st))) {
+        return rc;
+    }
     if ((rc = pcg_update_p(L.n, zz, ws.p, rho_new, rho_old, it == 1, st))) return rc;
     if ((rc = operator_apply(L.op, 3, ws.p, ws.w, st, ws.opws))) return rc;
     if ((rc = dot_dd(L.n, ws.p, ws.w, ws.partial, sc + S_CURV, st))) return rc;

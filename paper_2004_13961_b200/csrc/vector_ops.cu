@@ -30,6 +30,16 @@ __global__ void finalize_kernel(const double *__restrict__ partial, double *__re
     }
 }
 
+__global__ void sum_lines_kernel(const double *__restrict__ v, int64_t n, double *__restrict__ out) {
+    dd acc{0.0, 0.0};
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc = dd_add(acc, dd{v[i], 0.0});
+    acc = block_reduce_dd(acc);
+    if (threadIdx.x == 0) {
+        out[0] = acc.hi;
+        out[1] = acc.lo;
+    }
+}
+
 __global__ void update_p_kernel(int64_t n, const double *__restrict__ z, double *__restrict__ p,
                                 const double *__restrict__ rho_new,
                                 const double *__restrict__ rho_old, int first) {
@@ -77,6 +87,13 @@ unsigned grid_for(int64_t n) {
 
 int finalize_dd(const double *partial, double *out, cudaStream_t st) {
     finalize_kernel<<<1, 256, 0, st>>>(partial, out);
+    count_launch();
+    LP_CHECK_LAUNCH();
+    return LP_OK;
+}
+
+int sum_lines_dd(const double *v, int64_t n, double *out, cudaStream_t st) {
+    sum_lines_kernel<<<1, 1024, 0, st>>>(v, n, out);
     count_launch();
     LP_CHECK_LAUNCH();
     return LP_OK;

@@ -69,6 +69,8 @@ __device__ __forceinline__ dd block_reduce_dd(dd v) {
 int dot_dd(int64_t n, const double *a, const double *b, double *partial, double *out,
            cudaStream_t st);
 int finalize_dd(const double *partial, double *out, cudaStream_t st);
+// out (dd pair) = sum of v[0..n) in double-double, fixed order (one block)
+int sum_lines_dd(const double *v, int64_t n, double *out, cudaStream_t st);
 
 // p = first ? z : z + (rho_new / rho_old) * p   (pcg.py:150-155)
 int pcg_update_p(int64_t n, const double *z, double *p, const double *rho_new,

@@ -19,7 +19,7 @@ import numpy as np
 from . import _lib, device
 
 __all__ = ["SparseMatrix", "IluFactors", "IluZeroPivotError", "spmv", "ilu0",
-           "forward_sub", "backward_sub", "precond_apply", "save_matrix_market",
+           "forward_sub", "backward_sub", "precond_apply", "precond_apply_rz", "save_matrix_market",
            "load_matrix_market"]
 
 
@@ -235,6 +235,19 @@ def precond_apply(f, r):
     """One-step approximate solve of M z = r (sparse.py:219-221)."""
     x, dev = _vec(f, r, "precond_apply")
     return _run("lp_precond_apply", f._handle, x, f.n, dev)
+
+
+def precond_apply_rz(f, r):
+    """(z, r'z): the approximate solve M z = r together with the PCG scalar
+    rho = r'z of pcg.py:147-151, accumulated inside the backward sweep
+    (``lp_precond_apply_rz``; double-double, deterministic)."""
+    x, dev = _vec(f, r, "precond_apply")
+    out = device.empty(f.n)
+    rz = device.empty(2)
+    _lib.check(_lib.load().lp_precond_apply_rz(f._handle, x.data_ptr(), out.data_ptr(), rz.data_ptr(),
+                                               _lib.stream_ptr()), "precond_apply")
+    hi, lo = (float(v) for v in device.host(rz))
+    return (out if dev else device.host(out)), hi + lo
 
 
 def spmv(a, x):

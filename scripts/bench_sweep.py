@@ -37,3 +37,8 @@ for name in sys.argv[1:]:
     print(json.dumps({"cfg": name, "lib": os.path.basename(_lib.LIB_PATH), "assemble_s": t1 - t0,
                       "ilu0_s": t2 - t1, "fwd_s": tf, "bwd_s": tb,
                       "pair_gbs": B / (tf + tb) / 1e9, "nnz": nnz}), flush=True)
+    rz = torch.empty(2, dtype=torch.float64, device="cuda")
+    ta = time_events(torch, lambda: lib.lp_precond_apply(h, r.data_ptr(), z.data_ptr(), _lib.stream_ptr()), 5)
+    tz = time_events(torch, lambda: lib.lp_precond_apply_rz(h, r.data_ptr(), z.data_ptr(), rz.data_ptr(),
+                                                            _lib.stream_ptr()), 5)
+    print(json.dumps({"cfg": name, "precond_apply_s": ta, "precond_apply_rz_s": tz}), flush=True)

@@ -416,3 +416,23 @@ def test_assemble_rhs_matches_oracle():
     ospec = ProblemSpec(dim=2, N=w.N, beta=w.beta, alpha=w.alpha, rhs=f)
     ref = orc.assemble_rhs(ospec, orc.Plan(w.N + 1))
     assert relerr(got, ref) < 1e-13
+
+
+@pytest.mark.parametrize("name,N,T", [("cfg2", 64, 10), ("cfg2", 256, 10), ("cfg3", 150, 12),
+                                      ("cfg1", 128, 8), ("cfg4", 12, 8), ("cfg5", 14, 0)])
+def test_precond_apply_rz_fused(name, N, T):
+    """lp_precond_apply_rz: z equals precond_apply bit for bit and r'z (carried by
+    the backward sweep for the 1-D / 2-D boxes, pcg.py:147-151) matches the
+    long-double dot of the reference; the result is deterministic."""
+    from paper_2004_13961_b200.sparse import precond_apply_rz
+    w = wl.CONFIGS[name]()
+    f = ilu0(assemble_M(spec_of(w, N), T, T))
+    r = np.random.default_rng(3).standard_normal(f.n)
+    z0 = precond_apply(f, r)
+    z, rz = precond_apply_rz(f, r)
+    np.testing.assert_array_equal(z, z0)
+    ref = float(np.dot(r.astype(np.longdouble), z0.astype(np.longdouble)))
+    scale = float(np.dot(np.abs(r), np.abs(z0)))
+    assert abs(rz - ref) <= 1e-13 * scale
+    z2, rz2 = precond_apply_rz(f, r)
+    assert rz2 == rz
