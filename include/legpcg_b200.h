@@ -183,6 +183,35 @@ int lp_matrix_export(const lp_ilu *m, int which /*0=M,1=L,2=U*/, int64_t *indptr
  * reference would report (missing diagonal, |u_kk| < pivot_tol). */
 int lp_ilu0(lp_ilu *m, double pivot_tol, int64_t *bad_row, void *stream);
 
+/* ILU(0) of a 3-D box matrix distributed over nranks y-slab ranks (rank v owns
+ * the x-lines with y in [ys[v], ys[v+1]); the factorisation uses
+ * the sweeps' wavefront and the neighbours' U rows of the r halo lines).  A
+ * finished row goes to its owner's factor array and, its diagonal and upper
+ * planes, to every rank whose halo [ys[u] - r, ys[u+1] + r) contains its
+ * line, followed by that replica's line flag.  Every row's arithmetic is that
+ * of lp_ilu0 (sparse.py:116-139), so a rank's rows equal the single-GPU
+ * factors bit for bit.
+ *   lp_ilu0_ranks: one-device emulation, f[v] = rank v's matrix (each assembled
+ *     from the same problem), every rank in one launch, each reading only its
+ *     own array.
+ *   lp_ilu0_rank: one rank of a multi-GPU run (one process per GPU, launched
+ *     concurrently); peer_lu[v] / peer_flags[v]: rank v's factor and flag
+ *     arrays (lp_ilu_rank_arrays) mapped with lp_ipc_open -- required for the
+ *     slab neighbours; system-scope publication over NVLink. */
+int lp_ilu0_ranks(lp_ilu *const *f, int nranks, const int *ys, double pivot_tol,
+                  int64_t *bad_row, void *stream);
+int lp_ilu0_rank(lp_ilu *f, int nranks, const int *ys, int rank, double *const *peer_lu,
+                 int *const *peer_flags, double pivot_tol, int64_t *bad_row, void *stream);
+/* Multi-GPU set-up of lp_ilu0_rank, per rank: lp_ilu_rank_arrays gives the
+ * matrix IPC-exportable factor and flag arrays (before any factorisation) and
+ * their 64-byte CUDA IPC handles, which the ranks exchange and map with
+ * lp_ipc_open; lp_ilu0_rank_prepare copies M into the factor array and clears
+ * the flags; the ranks then synchronise (a barrier: a neighbour stores halo
+ * rows and flags into these arrays as soon as it starts) and call lp_ilu0_rank. */
+int lp_ilu_rank_arrays(lp_ilu *f, double **lu, int **flags, unsigned char *handle_lu64,
+                       unsigned char *handle_flags64);
+int lp_ilu0_rank_prepare(lp_ilu *f, int64_t *bad_row, void *stream);
+
 /* forward_sub / backward_sub / precond_apply (sparse.py:199-221). */
 int lp_forward_sub(lp_ilu *f, const double *r, double *y, void *stream);
 int lp_backward_sub(lp_ilu *f, const double *y, double *z, void *stream);

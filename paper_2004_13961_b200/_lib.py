@@ -59,6 +59,10 @@ _SIGS = {
     "lp_matrix_nnz": (_i32, [_vp, ctypes.POINTER(_i64)]),
     "lp_matrix_export": (_i32, [_vp, _i32, _vp, _vp, _vp]),
     "lp_ilu0": (_i32, [_vp, _dbl, ctypes.POINTER(_i64), _vp]),
+    "lp_ilu0_ranks": (_i32, [_vp, _i32, _vp, _dbl, ctypes.POINTER(_i64), _vp]),
+    "lp_ilu0_rank": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _dbl, ctypes.POINTER(_i64), _vp]),
+    "lp_ilu_rank_arrays": (_i32, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp]),
+    "lp_ilu0_rank_prepare": (_i32, [_vp, ctypes.POINTER(_i64), _vp]),
     "lp_forward_sub": (_i32, [_vp, _vp, _vp, _vp]),
     "lp_backward_sub": (_i32, [_vp, _vp, _vp, _vp]),
     "lp_precond_apply": (_i32, [_vp, _vp, _vp, _vp]),

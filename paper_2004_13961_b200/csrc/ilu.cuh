@@ -108,7 +108,20 @@ int box_build_even(lp_ilu *m, cudaStream_t st);
 int box_apply(lp_ilu *m, const double *r, double *z, const SweepScratch &s, cudaStream_t st);
 int box_ilu0_2d_tasks(lp_ilu *m, const double *src, double tol, unsigned long long *key, int *done,
                       cudaStream_t st);
-int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_t st);
+// y-slab rank layout of a multi-GPU ILU(0) (see ilu_box3d.cu): rank v factors the
+// x-lines with y in [ys[v], ys[v+1]) in lu[v]; own = -1 runs every rank in one
+// launch (emulation), own >= 0 one rank with its neighbours' arrays in lu/flags.
+struct IluRanks {
+    int nranks = 1, own = -1;
+    int ys[9] = {0};
+    double *lu[8] = {nullptr};
+    int *flags[8] = {nullptr};
+};
+int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_t st,
+                     const IluRanks *ranks = nullptr);
+int box_ilu0_prepare(lp_ilu *m, int64_t *bad_row, cudaStream_t st);
+int box_ilu0_ranks(lp_ilu *const *ms, int nranks, const int *ys, int own, double *const *peer_lu,
+                   int *const *peer_flags, double tol, int64_t *bad_row, cudaStream_t st);
 int box_ilu0_3d_blocks(lp_ilu *m, double tol, unsigned long long *key, cudaStream_t st);
 struct Geom;
 bool box_sweep3d_applies(const Geom &g);

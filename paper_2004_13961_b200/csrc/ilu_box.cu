@@ -722,6 +722,106 @@ int box_ilu0(lp_ilu *m, double tol, int64_t *bad_row, cudaStream_t st) {
     return box_build_bands(m, st);
 }
 
+// Factor storage of one rank ready for lp_ilu0_rank(s): M copied into the
+// factor array, line flags cleared (synchronises the stream).
+int box_ilu0_prepare(lp_ilu *m, int64_t *bad_row, cudaStream_t st) {
+    BoxLayout &b = m->box;
+    if (m->missing_diag >= 0) {
+        *bad_row = m->missing_diag;
+        set_error("zero pivot at elimination step %lld", (long long)*bad_row);
+        return LP_ERR_ZERO_PIVOT;
+    }
+    const size_t bytes = (size_t)b.n * b.S * sizeof(double);
+    if (!b.lu) {
+        if (dalloc(&b.lu, (size_t)b.n * b.S + 2, "ILU factors") != LP_OK) {
+            b.lu = b.values;
+            b.values = nullptr;
+        }
+    }
+    if (!b.values && m->factored) {
+        set_error("matrix was factored in place; re-assemble before refactoring");
+        return LP_ERR_ARG;
+    }
+    if (b.values) LP_CUDA(cudaMemcpyAsync(b.lu, b.values, bytes, cudaMemcpyDeviceToDevice, st));
+    LP_CUDA(cudaMemsetAsync(m->flags, 0, b.n * sizeof(int), st));
+    LP_CUDA(cudaStreamSynchronize(st));
+    return LP_OK;
+}
+
+// ILU(0) of a 3-D box matrix distributed over y-slab ranks (the
+// factorisation uses the sweeps' wavefront and needs the neighbours' U rows of
+// the r halo lines).  own = -1: ms[0..nranks) are the ranks' matrices (each
+// assembled from the same problem), factored in ONE launch on this device --
+// the emulation of the multi-GPU run, every rank reading only its own array
+// (its rows plus the halo rows its neighbours stored there).  own >= 0: ms[0]
+// is this rank's matrix; peer_lu / peer_flags hold the neighbours' factor and
+// flag arrays mapped over CUDA IPC (entries of non-neighbours may be null).
+// Every row's arithmetic is the single-GPU kernel's: the owners' rows equal the
+// single-GPU factors bit for bit.
+int box_ilu0_ranks(lp_ilu *const *ms, int nranks, const int *ys, int own, double *const *peer_lu,
+                   int *const *peer_flags, double tol, int64_t *bad_row, cudaStream_t st) {
+    LP_ARG(nranks >= 1 && nranks <= 8, "1 to 8 ranks");
+    const int nh = own >= 0 ? 1 : nranks;
+    lp_ilu *m0 = ms[0];
+    Geom g = geom_of(m0->box);
+    LP_ARG(g.d == 3 && g.r >= 1 && g.r <= 10 && m0->box.mask, "the distributed ILU(0) serves 3-D boxes of reach 1..10");
+    LP_ARG(ys[0] == 0 && ys[nranks] == g.K, "ys must split [0, K)");
+    for (int v = 0; v < nranks; ++v) LP_ARG(ys[v + 1] > ys[v], "empty y-slab");
+    IluRanks rk;
+    rk.nranks = nranks;
+    rk.own = own;
+    for (int v = 0; v <= nranks; ++v) rk.ys[v] = ys[v];
+    *bad_row = -1;
+    for (int h = 0; h < nh; ++h) {
+        lp_ilu *m = ms[h];
+        BoxLayout &b = m->box;
+        LP_ARG(m->kind == MAT_BOX && b.n == m0->box.n && b.r == g.r, "rank matrices differ");
+        // one rank of a multi-GPU run is prepared (and the ranks synchronised) by the
+        // caller: a neighbour may already be storing halo rows and flags here
+        if (own < 0) {
+            const int rp = box_ilu0_prepare(m, bad_row, st);
+            if (rp) return rp;
+        } else {
+            LP_ARG(b.lu != nullptr, "call lp_ilu0_rank_prepare (and synchronise the ranks) first");
+        }
+        const int v = own >= 0 ? own : h;
+        rk.lu[v] = b.lu;
+        rk.flags[v] = m->flags;
+    }
+    if (own >= 0)
+        for (int v = 0; v < nranks; ++v)
+            if (v != own) {
+                rk.lu[v] = peer_lu ? peer_lu[v] : nullptr;
+                rk.flags[v] = peer_flags ? peer_flags[v] : nullptr;
+                const bool neighbour = v == own - 1 || v == own + 1;
+                LP_ARG(!neighbour || (rk.lu[v] && rk.flags[v]), "the slab neighbours' arrays are required");
+            }
+    unsigned long long *key = reinterpret_cast<unsigned long long *>(m0->bad);
+    const unsigned long long none = ~0ull;
+    LP_CUDA(cudaMemcpyAsync(key, &none, sizeof none, cudaMemcpyHostToDevice, st));
+    LP_CUDA(cudaMemsetAsync(m0->ticket, 0, sizeof(int), st));
+    int rc = box_ilu0_3d_rows(m0, tol, key, st, &rk);
+    if (rc != LP_OK) return rc;
+    unsigned long long hk;
+    LP_CUDA(cudaMemcpyAsync(&hk, key, sizeof hk, cudaMemcpyDeviceToHost, st));
+    LP_CUDA(cudaStreamSynchronize(st));
+    if (hk != none) {
+        *bad_row = (int64_t)(hk % (unsigned long long)g.n);
+        set_error("zero pivot at elimination step %lld (row %lld)", (long long)*bad_row,
+                  (long long)(hk / (unsigned long long)g.n));
+        return LP_ERR_ZERO_PIVOT;
+    }
+    for (int h = 0; h < nh; ++h) {
+        lp_ilu *m = ms[h];
+        LP_CUDA(cudaMemsetAsync(m->flags, 0, m->box.n * sizeof(int), st));
+        m->epoch = 0;
+        m->factored = true;
+        if ((rc = box_build_bands(m, st))) return rc;
+    }
+    LP_CUDA(cudaStreamSynchronize(st));
+    return LP_OK;
+}
+
 int box_export(const lp_ilu *m, int which, int64_t *indptr, int32_t *indices, double *values) {
     const BoxLayout &b = m->box;
     const double *src = which == 0 ? b.values : b.lu;

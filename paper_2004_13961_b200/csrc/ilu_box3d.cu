@@ -96,7 +96,30 @@ struct Ilu3Args {
     const int *line_order;
     const int *lvl_first;
     const long long *lvl_start;
+    // y-slab ranks (multi-GPU factorisation): rank v owns the x-lines
+    // with y in [ys[v], ys[v+1]) and factors them in ITS factor array lu_r[v]
+    // (global row indexing; only its own rows and the halo lines
+    // [ys[v] - r, ys[v+1] + r) are ever valid there).  A finished row is stored
+    // to its owner and -- its diagonal/upper planes, the part pivots read -- to
+    // every rank whose halo contains its line, followed by that replica's
+    // line flag.  nranks = 1: lu_r[0] = lu, flags_r[0] = lineflags.
+    // own = -1: every rank in this launch (one-device emulation); own >= 0: this
+    // launch factors rank `own` only, the other entries are its neighbours'
+    // arrays mapped over CUDA IPC (system-scope publication).
+    int nranks, own;
+    int ys[9];
+    double *lu_r[8];
+    int *flags_r[8];
 };
+
+__device__ __forceinline__ void st_release_sys(int *p, int v) {
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_sys(const int *p) {
+    int v;
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
 __device__ __forceinline__ unsigned long long gtime3() {
     unsigned long long t;
@@ -178,10 +201,17 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
         if (i >= n) return;
         const int ix = (int)(i % K);
         const int64_t L = i / K;
+        // the row's owner among the y-slab ranks, and that rank's arrays
+        const int iyr = (int)(L % K);
+        int rk = 0;
+        while (rk + 1 < a.nranks && iyr >= a.ys[rk + 1]) ++rk;
+        if (a.own >= 0 && rk != a.own) continue;   // another rank's row (uniform)
+        double *const lu = a.lu_r[rk];
+        int *const lineflags = a.flags_r[rk];
 #ifdef LP_ILU_TRACE
         if (tid == 0) a.trace[i * 8] = gtime3();
 #endif
-        double *gi = a.lu + (size_t)i * S;
+        double *gi = lu + (size_t)i * S;
         for (int q = tid; q < mw; q += TPB) bits[q] = a.mask[(size_t)i * mw + q];
         double v[W];
 #pragma unroll
@@ -246,21 +276,21 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
                 const int64_t Lk = L + py + (int64_t)K * pz;
                 const int lid = pz * W + py;
                 if (lid == 0) {
-                    while (ld_acquire(a.lineflags + Lk) < ix + px + 1) {
+                    while ((a.own >= 0 ? ld_acquire_sys(lineflags + Lk) : ld_acquire(lineflags + Lk)) < ix + px + 1) {
 #ifdef LP_ILU_TRACE
                         ++spin_in;
 #endif
                     }
                 } else if (lid != ready_line) {
                     const int need = min(K, ix + R + 1);
-                    while (ld_acquire(a.lineflags + Lk) < need) {
+                    while ((a.own >= 0 ? ld_acquire_sys(lineflags + Lk) : ld_acquire(lineflags + Lk)) < need) {
 #ifdef LP_ILU_TRACE
                         ++spin_line;
 #endif
                     }
                     ready_line = lid;
                 }
-                const double *uk = a.lu + (size_t)(i + px + (int64_t)K * (py + (int64_t)K * pz)) * S;
+                const double *uk = lu + (size_t)(i + px + (int64_t)K * (py + (int64_t)K * pz)) * S;
                 const int slot = pn % D;
                 if (tid == (py + R) * W + (px + R)) cp_async8(spiv_s + slot * 8, uk + C);
                 if (col && abs(tx - px) <= R && abs(ty - py) <= R) {
@@ -374,13 +404,33 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
 #pragma unroll
             for (int z = 0; z < W; ++z) __stcg(gi + tid + z * W2, v[z]);
         }
-        __threadfence();
+        // halo: the planes pivots read (diagonal and above) into the neighbours' arrays
+        unsigned halo = 0;
+        for (int u = 0; u < a.nranks; ++u)
+            if (u != rk && iyr >= a.ys[u] - R && iyr < a.ys[u + 1] + R) halo |= 1u << u;
+        for (int u = 0; u < a.nranks; ++u)
+            if ((halo >> u) & 1u) {
+                double *gu = a.lu_r[u] + (size_t)i * S;
+                if (col) {
+#pragma unroll
+                    for (int z = R; z < W; ++z) __stcg(gu + tid + z * W2, v[z]);
+                }
+            }
+        if (halo && a.own >= 0) __threadfence_system();
+        else __threadfence();
         __syncthreads();
         if (tid == 0) {
-            // publish the line's contiguous prefix (row x - 1 publishes first)
-            while (ld_acquire(a.lineflags + L) != ix) {
+            // publish the line's contiguous prefix (row x - 1 publishes first): the
+            // neighbours' replicas before the owner's flag, which is what releases
+            // row x + 1 -- so every replica's prefix grows in order too
+            while (ld_acquire(lineflags + L) != ix) {
             }
-            st_release(a.lineflags + L, ix + 1);
+            for (int u = 0; u < a.nranks; ++u)
+                if ((halo >> u) & 1u) {
+                    if (a.own >= 0) st_release_sys(a.flags_r[u] + L, ix + 1);
+                    else st_release(a.flags_r[u] + L, ix + 1);
+                }
+            st_release(lineflags + L, ix + 1);
 #ifdef LP_ILU_TRACE
             a.trace[i * 8 + 3] = gtime3();
             a.trace[i * 8 + 4] = spin_line;
@@ -415,12 +465,12 @@ int launch3(const Ilu3Args &a, cudaStream_t st) {
 
 // Launches the 3-D row kernel; returns a negative code when it does not apply
 // (r outside 1..10), in which case the caller uses the generic kernel.
-int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_t st) {
+int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_t st, const IluRanks *ranks) {
     BoxLayout &b = m->box;
     Geom g = geom_of(b);
     if (g.d != 3) return LP_ERR_ARG;
     // large reach: blocks of x-adjacent rows share their pivot rows (ilu_box3d_blk.cu)
-    if (g.r >= LP_ILU3_BLK_MIN_R && box_ilu0_3d_blocks(m, tol, key, st) == LP_OK) return LP_OK;
+    if (!ranks && g.r >= LP_ILU3_BLK_MIN_R && box_ilu0_3d_blocks(m, tol, key, st) == LP_OK) return LP_OK;
     Ilu3Args a;
     a.g = g;
     a.lu = b.lu;
@@ -433,6 +483,21 @@ int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_
     a.line_order = nullptr;
     a.lvl_first = nullptr;
     a.lvl_start = nullptr;
+    a.nranks = 1;
+    a.own = -1;
+    a.ys[0] = 0;
+    a.ys[1] = g.K;
+    a.lu_r[0] = b.lu;
+    a.flags_r[0] = m->flags;
+    if (ranks) {
+        a.nranks = ranks->nranks;
+        a.own = ranks->own;
+        for (int v = 0; v <= ranks->nranks; ++v) a.ys[v] = ranks->ys[v];
+        for (int v = 0; v < ranks->nranks; ++v) {
+            a.lu_r[v] = ranks->lu[v];
+            a.flags_r[v] = ranks->flags[v];
+        }
+    }
     // Level order: row (x, y, z) can run at level x + (r+1)(y + (r+1)z) and every
     // row it depends on has a smaller level, so handing rows out by level is
     // deadlock-free while spreading the rows in flight over many x-lines (natural

@@ -15,6 +15,8 @@
 
 #include <vector>
 
+#include <string.h>
+
 #include "ilu.cuh"
 #include "vector_ops.cuh"
 
@@ -358,6 +360,55 @@ static int with_scratch(lp_ilu *m, cudaStream_t st, F &&body) {
     if (!rc) rc = body(s);
     scratch_free(s, st);
     return rc;
+}
+
+extern "C" int lp_ilu0_ranks(lp_ilu *const *ms, int nranks, const int *ys, double tol, int64_t *bad_row,
+                             void *stream) {
+    return box_ilu0_ranks(ms, nranks, ys, -1, nullptr, nullptr, tol, bad_row, as_stream(stream));
+}
+
+extern "C" int lp_ilu0_rank(lp_ilu *m, int nranks, const int *ys, int rank, double *const *peer_lu,
+                            int *const *peer_flags, double tol, int64_t *bad_row, void *stream) {
+    LP_ARG(rank >= 0 && rank < nranks, "rank out of range");
+    lp_ilu *ms[1] = {m};
+    return box_ilu0_ranks(ms, nranks, ys, rank, peer_lu, peer_flags, tol, bad_row, as_stream(stream));
+}
+
+extern "C" int lp_ilu_rank_arrays(lp_ilu *m, double **lu, int **flags, unsigned char *handle_lu64,
+                                  unsigned char *handle_flags64) {
+    LP_ARG(m->kind == MAT_BOX, "box matrices only");
+    lp::BoxLayout &b = m->box;
+    LP_ARG(b.lu == nullptr, "call before the matrix is factored");
+    // plain cudaMalloc memory: stream-ordered pool allocations cannot be exported over CUDA IPC
+    double *nlu = nullptr;
+    int *nfl = nullptr;
+    LP_CUDA(cudaMalloc(&nlu, ((size_t)b.n * b.S + 2) * sizeof(double)));
+    cudaError_t e = cudaMalloc(&nfl, (size_t)b.n * sizeof(int));
+    if (e != cudaSuccess) {
+        cudaFree(nlu);
+        return cuda_fail(e, "rank flag array", __FILE__, __LINE__);
+    }
+    cudaIpcMemHandle_t h1, h2;
+    if ((e = cudaIpcGetMemHandle(&h1, nlu)) != cudaSuccess || (e = cudaIpcGetMemHandle(&h2, nfl)) != cudaSuccess) {
+        cudaFree(nlu);
+        cudaFree(nfl);
+        return cuda_fail(e, "IPC export of the rank arrays", __FILE__, __LINE__);
+    }
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    memcpy(handle_lu64, &h1, 64);
+    memcpy(handle_flags64, &h2, 64);
+    dfree(m->flags);
+    m->flags = nfl;
+    b.lu = nlu;
+    *lu = nlu;
+    *flags = nfl;
+    return LP_OK;
+}
+
+extern "C" int lp_ilu0_rank_prepare(lp_ilu *m, int64_t *bad_row, void *stream) {
+    LP_ARG(m->kind == MAT_BOX, "box matrices only");
+    *bad_row = -1;
+    return box_ilu0_prepare(m, bad_row, as_stream(stream));
 }
 
 extern "C" int lp_forward_sub(lp_ilu *m, const double *r, double *y, void *stream) {

@@ -247,6 +247,76 @@ class SlabSweeps:
         return out
 
 
+def ilu0_sharded_local(matrices, pivot_tol=1e-300):
+    """ILU(0) over G y-slab ranks, emulated on one device (``lp_ilu0_ranks``):
+    ``matrices[v]`` is rank v's assembled M (``assemble_M`` of the same problem,
+    one per rank, as each GPU of a multi-GPU run assembles its own).  Every
+    rank factors the x-lines with y in its slab in its own factor array,
+    reading its neighbours' rows of the r halo lines from the copies they
+    stored there (sparse.py:116-139 per row).  Returns one
+    ``IluFactors`` per rank: the rows of the rank's slab equal the single-GPU
+    factors bit for bit; rows outside its slab are not factors."""
+    import ctypes
+    from .sparse import IluFactors, IluZeroPivotError
+    G = len(matrices)
+    K = round(matrices[0].n ** (1.0 / 3.0))
+    ys = [y0 for y0, _ in slab_bounds(K, G)] + [K]
+    cys = (ctypes.c_int * (G + 1))(*ys)
+    hs = (ctypes.c_void_p * G)(*[m._handle for m in matrices])
+    bad = ctypes.c_int64(-1)
+    rc = _lib.load().lp_ilu0_ranks(hs, G, cys, pivot_tol, ctypes.byref(bad), _lib.stream_ptr())
+    if rc == _lib.LP_ERR_ZERO_PIVOT:
+        raise IluZeroPivotError(int(bad.value))
+    _lib.check(rc, "ilu0 (y-slab ranks)")
+    return [IluFactors(m, m._handle) for m in matrices], ys
+
+
+def ilu0_rank(matrix, rank, G, group=None, pivot_tol=1e-300):
+    """This process's part of the ILU(0) over G y-slab ranks (one process per
+    GPU, ``lp_ilu0_rank``): ``matrix`` is this rank's assembled M.  The ranks
+    exchange the CUDA IPC handles of their factor and flag arrays, map their
+    slab neighbours', synchronise and factor concurrently; a finished halo row
+    is stored into the neighbour's array over NVLink, followed by its flag.
+    Returns this rank's ``IluFactors`` (its slab's rows are the single-GPU
+    factors bit for bit)."""
+    import ctypes
+
+    import torch.distributed as dist
+    from .sparse import IluFactors, IluZeroPivotError
+    lib = _lib.load()
+    K = round(matrix.n ** (1.0 / 3.0))
+    ys = [y0 for y0, _ in slab_bounds(K, G)] + [K]
+    cys = (ctypes.c_int * (G + 1))(*ys)
+    lu, fl = ctypes.c_void_p(), ctypes.c_void_p()
+    h_lu, h_fl = (ctypes.c_ubyte * 64)(), (ctypes.c_ubyte * 64)()
+    _lib.check(lib.lp_ilu_rank_arrays(matrix._handle, ctypes.byref(lu), ctypes.byref(fl), h_lu, h_fl),
+               "rank arrays")
+    allh = [None] * G
+    dist.all_gather_object(allh, (bytes(h_lu), bytes(h_fl)), group=group)
+    peer_lu, peer_fl, opened = (ctypes.c_void_p * G)(), (ctypes.c_void_p * G)(), []
+    for v in range(G):
+        if abs(v - rank) == 1:
+            for which, dst in ((0, peer_lu), (1, peer_fl)):
+                p = ctypes.c_void_p()
+                hb = (ctypes.c_ubyte * 64).from_buffer_copy(allh[v][which])
+                _lib.check(lib.lp_ipc_open(hb, ctypes.byref(p)), "ipc open")
+                dst[v] = p.value
+                opened.append(p.value)
+    bad = ctypes.c_int64(-1)
+    rc = lib.lp_ilu0_rank_prepare(matrix._handle, ctypes.byref(bad), _lib.stream_ptr())
+    dist.barrier(group=group)   # every rank's arrays are ready before any halo store
+    if rc == _lib.LP_OK:
+        rc = lib.lp_ilu0_rank(matrix._handle, G, cys, rank, peer_lu, peer_fl, pivot_tol,
+                              ctypes.byref(bad), _lib.stream_ptr())
+    dist.barrier(group=group)   # the neighbours are done storing into this rank's arrays
+    for p in opened:
+        lib.lp_ipc_close(p)
+    if rc == _lib.LP_ERR_ZERO_PIVOT:
+        raise IluZeroPivotError(int(bad.value))
+    _lib.check(rc, "ilu0 (rank)")
+    return IluFactors(matrix, matrix._handle)
+
+
 # ------------------------------------------------------------ PCG driver
 #
 # One PCG loop (pcg.py:145-164) written against per-slab operations, run either

@@ -31,6 +31,8 @@ ap.add_argument("--workload", default="cfg4")
 ap.add_argument("--N", type=int)
 ap.add_argument("--T", type=int)
 ap.add_argument("--check", action="store_true")
+ap.add_argument("--rank-ilu", action="store_true",
+                help="factor with the distributed ILU(0) (ilu0_rank: each rank its y-slab, halo rows over CUDA IPC)")
 args = ap.parse_args()
 local = int(os.environ.get("LOCAL_RANK", "0"))
 torch.cuda.set_device(local)
@@ -48,18 +50,24 @@ f_slab = device.to_device(F[z0 * K * K:(z0 + nz) * K * K])
 torch.cuda.synchronize()
 dist.barrier()
 t0 = time.perf_counter()
-fac = setup_preconditioner(spec, cfg, plan)
+if args.rank_ilu:
+    from paper_2004_13961_b200 import assemble_M
+    from paper_2004_13961_b200.sharded import ilu0_rank
+    fac = ilu0_rank(assemble_M(spec, w.T, w.T, plan), rank, G)
+else:
+    fac = setup_preconditioner(spec, cfg, plan)
 torch.cuda.synchronize()
 t1 = time.perf_counter()
 x, rep = pcg_solve_sharded_rank(spec, cfg, plan, f_slab, factors=fac)
 torch.cuda.synchronize()
 t2 = time.perf_counter()
-out = {"workload": args.workload, "N": w.N, "T": w.T, "ranks": G, "iterations": rep["iterations"],
+out = {"workload": args.workload, "N": w.N, "T": w.T, "ranks": G, "rank_ilu": bool(args.rank_ilu), "iterations": rep["iterations"],
        "converged": rep["converged"], "relres": rep["final_relative_residual"],
        "setup_s": max_over_ranks(t1 - t0, "cuda"), "loop_s": max_over_ranks(t2 - t1, "cuda")}
 if args.check:
     from paper_2004_13961_b200.pcg import pcg_solve_device
-    x1, _ = pcg_solve_device(spec, cfg, plan, device.to_device(F), factors=fac)
+    fac1 = setup_preconditioner(spec, cfg, plan) if args.rank_ilu else fac
+    x1, _ = pcg_solve_device(spec, cfg, plan, device.to_device(F), factors=fac1)
     mine = x1[z0 * K * K:(z0 + nz) * K * K]
     num = torch.linalg.vector_norm(x - mine) ** 2
     den = torch.linalg.vector_norm(mine) ** 2

@@ -467,3 +467,31 @@ def test_box_sweeps_match_csr_sweeps(name, N, T):
     r = np.random.default_rng(9).standard_normal(m.n)
     zb, zc = precond_apply(fb, r), precond_apply(fc, r)
     assert relerr(zb, zc) < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,N,T,G", [("cfg5", 16, 2, 2), ("cfg5", 16, 2, 3), ("cfg4", 14, 8, 2),
+                                        ("cfg5", 20, 0, 4), ("cfg4", 24, 6, 3), ("cfg5", 26, 8, 2)])
+def test_distributed_ilu0_bitwise(name, N, T, G):
+    """ILU(0) over G y-slab ranks (lp_ilu0_ranks, one-device emulation of the
+    multi-GPU factorisation: every rank reads only its own factor array, its
+    neighbours' halo rows arrive as stores): the rows of every rank's slab equal
+    the single-GPU factors bit for bit (sparse.py:116-139 per row)."""
+    from paper_2004_13961_b200 import ProblemSpec, TransformPlan, assemble_M, ilu0, workloads as wl
+    from paper_2004_13961_b200.sharded import ilu0_sharded_local
+    w = wl.CONFIGS[name]()
+    spec = ProblemSpec(dim=3, N=N, beta=w.beta, alpha=w.alpha)
+    plan = TransformPlan(N + 1)
+    K = N - 1
+    ref = ilu0(assemble_M(spec, T, T, plan))
+    facs, ys = ilu0_sharded_local([assemble_M(spec, T, T, plan) for _ in range(G)])
+    for part in ("L", "U"):
+        rp = getattr(ref, part)
+        for v, f in enumerate(facs):
+            fp = getattr(f, part)
+            np.testing.assert_array_equal(fp.indptr, rp.indptr)
+            rows = np.arange(K ** 3)
+            own = ((rows // K) % K >= ys[v]) & ((rows // K) % K < ys[v + 1])
+            sel = np.repeat(own, np.diff(rp.indptr))
+            np.testing.assert_array_equal(fp.values[sel], rp.values[sel])
+            assert sel.any()
