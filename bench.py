@@ -415,11 +415,13 @@ def cpu_full_matvec_s(workload):
 
 def sample_text(workload, N, it, t):
     w, _ = build_workload(workload, N)
-    return (f"full ILU(0)-PCG solve of the {workload} coefficient recipe at N={N} "
+    head = (f"full ILU(0)-PCG solve of the {workload} coefficient recipe at N={N} "
             f"(T={w.T}, rtol {w.rtol:g}, {it} iterations, {t:.1f} s): oracle port of the reference, "
-            "numpy/OpenBLAS on all host cores + single-threaded C ILU(0)/sweeps; the full-size "
-            f"{workload} solve does not fit a CPU host (SURVEY 8(c)), so this bounded sample stands "
-            "in for it (CPU cost per DOF grows with N: conservative)")
+            "numpy/OpenBLAS on all host cores + single-threaded C ILU(0)/sweeps")
+    if N == {"cfg1": 128, "cfg2": 256, "cfg3": 2048, "cfg4": 128, "cfg5": 512}.get(workload):
+        return head + "; this is the full-size workload"
+    return (head + f"; the full-size {workload} solve does not fit a CPU host (SURVEY 8(c)), so this "
+            "bounded sample stands in for it (CPU cost per DOF grows with N: conservative)")
 
 
 def run_reference(args, ws, rank):

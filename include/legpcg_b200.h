@@ -257,6 +257,31 @@ int lp_update_xr(int64_t n, double *x, double *r, const double *p, const double 
                  double *out2, void *stream);
 int lp_dot(int64_t n, const double *a, const double *b, double *out2, void *stream);
 
+/* ------------------------------------------------------------ multi-GPU --
+ * Collectives of the distributed solve on the caller's NCCL communicator
+ * (one process per GPU).  nccl_comm is an ncclComm_t; NCCL is
+ * resolved at run time from the libnccl.so.2 the process already uses, the
+ * library does not link it.  slab_axis: the axis the vectors are split along
+ * (2 = z-slabs, the layout of the sharded matvec).  The communicator stays
+ * the caller's.
+ *   lp_comm_allreduce_dd: the PCG scalars r'z, p'w, r'r (pcg.py:150-159) --
+ *     dd_inout (device, a double-double pair) is all-gathered and summed in
+ *     rank order, so every rank holds the same bits.
+ *   lp_comm_dot: this rank's deterministic double-double dot (lp_dot) followed
+ *     by lp_comm_allreduce_dd.
+ *   lp_comm_alltoall: the transposes of the slab-sharded apply_system
+ *     (operator.py:204-210 across ranks): chunk v of `send` (send_counts[v]
+ *     doubles, chunks in rank order) goes to rank v, chunk v of `recv` comes
+ *     from rank v; counts are host arrays of `size` entries. */
+typedef struct lp_comm lp_comm;
+int lp_comm_init(void *nccl_comm, int rank, int size, int slab_axis, lp_comm **out);
+int lp_comm_destroy(lp_comm *comm);
+int lp_comm_allreduce_dd(lp_comm *comm, double *dd_inout, void *stream);
+int lp_comm_dot(lp_comm *comm, int64_t n, const double *a, const double *b, double *out2,
+                void *stream);
+int lp_comm_alltoall(lp_comm *comm, const double *send, const int64_t *send_counts, double *recv,
+                     const int64_t *recv_counts, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

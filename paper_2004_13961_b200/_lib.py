@@ -84,6 +84,11 @@ _SIGS = {
     "lp_update_xr": (_i32, [_i64, _vp, _vp, _vp, _vp, _dbl, _vp, _vp]),
     "lp_slab_forward": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "lp_slab_middle": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "lp_comm_init": (_i32, [_vp, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
+    "lp_comm_destroy": (_i32, [_vp]),
+    "lp_comm_allreduce_dd": (_i32, [_vp, _vp, _vp]),
+    "lp_comm_dot": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp]),
+    "lp_comm_alltoall": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "lp_slab_backward": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
 }
 

@@ -495,3 +495,61 @@ def test_distributed_ilu0_bitwise(name, N, T, G):
             sel = np.repeat(own, np.diff(rp.indptr))
             np.testing.assert_array_equal(fp.values[sel], rp.values[sel])
             assert sel.any()
+
+
+@pytest.mark.gpu
+def test_comm_abi_one_rank_nccl():
+    """lp_comm_* (the C-ABI collectives on a caller-owned ncclComm_t) with a
+    one-rank communicator created straight from libnccl: the rank-ordered
+    double-double allreduce is the identity, lp_comm_dot equals lp_dot bit for
+    bit, and the all-to-all moves the own chunk."""
+    import ctypes
+    from paper_2004_13961_b200 import _lib
+    lib = _lib.load()
+    torch.zeros(1, device="cuda")
+    nccl = None
+    for name in ("libnccl.so.2", "libnccl.so"):
+        try:
+            nccl = ctypes.CDLL(name)
+            break
+        except OSError:
+            continue
+    if nccl is None:
+        import glob
+        import os
+        cands = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "nccl", "lib",
+                                       "libnccl.so.2"))
+        assert cands, "no libnccl.so.2"
+        nccl = ctypes.CDLL(cands[0], mode=ctypes.RTLD_GLOBAL)
+    uid = (ctypes.c_byte * 128)()
+    assert nccl.ncclGetUniqueId(ctypes.byref(uid)) == 0
+    comm = ctypes.c_void_p()
+
+    class Uid(ctypes.Structure):
+        _fields_ = [("internal", ctypes.c_byte * 128)]
+    nccl.ncclCommInitRank.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, Uid, ctypes.c_int]
+    u = Uid()
+    ctypes.memmove(ctypes.byref(u), uid, 128)
+    assert nccl.ncclCommInitRank(ctypes.byref(comm), 1, u, 0) == 0
+    h = ctypes.c_void_p()
+    try:
+        _lib.check(lib.lp_comm_init(comm, 0, 1, 2, ctypes.byref(h)), "comm init")
+        st = _lib.stream_ptr()
+        n = 100003
+        a = torch.randn(n, dtype=torch.float64, device="cuda")
+        b = torch.randn(n, dtype=torch.float64, device="cuda")
+        d1 = torch.empty(2, dtype=torch.float64, device="cuda")
+        d2 = torch.empty(2, dtype=torch.float64, device="cuda")
+        _lib.check(lib.lp_dot(n, a.data_ptr(), b.data_ptr(), d1.data_ptr(), st))
+        _lib.check(lib.lp_comm_dot(h, n, a.data_ptr(), b.data_ptr(), d2.data_ptr(), st))
+        assert torch.equal(d1, d2)
+        cnt = (ctypes.c_int64 * 1)(n)
+        out = torch.zeros_like(a)
+        _lib.check(lib.lp_comm_alltoall(h, a.data_ptr(), cnt, out.data_ptr(), cnt, st))
+        torch.cuda.synchronize()
+        assert torch.equal(out, a)
+    finally:
+        if h.value:
+            lib.lp_comm_destroy(h)
+        nccl.ncclCommDestroy.argtypes = [ctypes.c_void_p]
+        nccl.ncclCommDestroy(comm)
