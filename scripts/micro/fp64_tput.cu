@@ -22,10 +22,9 @@ __global__ void __launch_bounds__(512, 1) tput(double *out, double a, double b, 
 }
 
 template <int MODE>
-void run(const char *name, int threads, double ops_per_iter) {
+void run(const char *name, int threads, double ops_per_iter, int n = 20000) {
     double *out;
     cudaMalloc(&out, 148 * 1024 * 8);
-    const int n = 20000;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -47,5 +46,9 @@ int main() {
     run<0>("DFMA", 128, 1);
     run<2>("DMUL(hoisted)+DADD", 512, 1);
     run<1>("DMUL+DADD", 512, 3);
+    // sustained: seconds, not milliseconds (power / clock behaviour under a long FP64 load)
+    run<0>("DFMA sustained", 512, 1, 4000000);
+    run<2>("DADD sustained", 512, 1, 4000000);
+    run<0>("DFMA sustained", 512, 1, 20000000);
     return 0;
 }
