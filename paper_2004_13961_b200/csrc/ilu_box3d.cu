@@ -46,10 +46,6 @@
 
 namespace lp {
 
-#ifdef LP_ILU_TRACE
-unsigned long long *g_ilu_trace = nullptr;   // dev builds: row timestamps of the last factorisation
-size_t g_ilu_trace_n = 0;
-#endif
 
 namespace {
 
@@ -89,7 +85,6 @@ struct Ilu3Args {
     int *ticket;
     double tol;
     unsigned long long *bad;
-    unsigned long long *trace;   // LP_ILU_TRACE builds: [n][4] timestamps
     // level order (null: natural order): ticket t -> level l with
     // lvl_start[l] <= t < lvl_start[l+1]; its o-th row lies on x-line
     // line_order[lvl_first[l] + o] at x = l - (r+1) key(line)
@@ -119,12 +114,6 @@ __device__ __forceinline__ int ld_acquire_sys(const int *p) {
     int v;
     asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
-}
-
-__device__ __forceinline__ unsigned long long gtime3() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
 }
 
 __device__ __forceinline__ bool bit_of(const uint32_t *bits, int t) {
@@ -208,9 +197,6 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
         if (a.own >= 0 && rk != a.own) continue;   // another rank's row (uniform)
         double *const lu = a.lu_r[rk];
         int *const lineflags = a.flags_r[rk];
-#ifdef LP_ILU_TRACE
-        if (tid == 0) a.trace[i * 8] = gtime3();
-#endif
         double *gi = lu + (size_t)i * S;
         for (int q = tid; q < mw; q += TPB) bits[q] = a.mask[(size_t)i * mw + q];
         double v[W];
@@ -265,9 +251,6 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
         // ---- prefetch: stages pivot pn into ring slot pn % D
         int pn = 0;
         int ready_line = -1 << 20;
-#ifdef LP_ILU_TRACE
-        unsigned long long spin_in = 0, spin_line = 0;
-#endif
         auto prefetch = [&]() {
             if (pn < npiv) {
                 const int e = plist[pn];
@@ -277,16 +260,10 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
                 const int lid = pz * W + py;
                 if (lid == 0) {
                     while ((a.own >= 0 ? ld_acquire_sys(lineflags + Lk) : ld_acquire(lineflags + Lk)) < ix + px + 1) {
-#ifdef LP_ILU_TRACE
-                        ++spin_in;
-#endif
                     }
                 } else if (lid != ready_line) {
                     const int need = min(K, ix + R + 1);
                     while ((a.own >= 0 ? ld_acquire_sys(lineflags + Lk) : ld_acquire(lineflags + Lk)) < need) {
-#ifdef LP_ILU_TRACE
-                        ++spin_line;
-#endif
                     }
                     ready_line = lid;
                 }
@@ -392,14 +369,8 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
                 ++en;
                 prefetch();
             }
-#ifdef LP_ILU_TRACE
-            if (pzi == R - 1 && tid == 0) a.trace[i * 8 + 1] = gtime3();
-#endif
         }
         cp_wait<0>();
-#ifdef LP_ILU_TRACE
-        if (tid == 0) a.trace[i * 8 + 2] = gtime3();
-#endif
         if (col) {
 #pragma unroll
             for (int z = 0; z < W; ++z) __stcg(gi + tid + z * W2, v[z]);
@@ -431,12 +402,6 @@ __global__ void __launch_bounds__(Cfg<R>::TPB, 1) box_ilu0_3d_kernel(const __gri
                     else st_release(a.flags_r[u] + L, ix + 1);
                 }
             st_release(lineflags + L, ix + 1);
-#ifdef LP_ILU_TRACE
-            a.trace[i * 8 + 3] = gtime3();
-            a.trace[i * 8 + 4] = spin_line;
-            a.trace[i * 8 + 5] = spin_in;
-            a.trace[i * 8 + 6] = (unsigned long long)npiv;
-#endif
         }
     }
 }
@@ -479,7 +444,6 @@ int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_
     a.ticket = m->ticket;
     a.tol = tol;
     a.bad = key;
-    a.trace = nullptr;
     a.line_order = nullptr;
     a.lvl_first = nullptr;
     a.lvl_start = nullptr;
@@ -534,21 +498,6 @@ int box_ilu0_3d_rows(lp_ilu *m, double tol, unsigned long long *key, cudaStream_
         a.lvl_first = lvl_first;
         a.lvl_start = lvl_start;
     }
-#ifdef LP_ILU_TRACE
-    {
-        static unsigned long long *tr = nullptr;
-        static size_t trn = 0;
-        if (trn < (size_t)g.n * 8) {
-            if (tr) dfree(tr);
-            trn = (size_t)g.n * 8;
-            dalloc(&tr, trn, "ilu trace");
-        }
-        cudaMemsetAsync(tr, 0, trn * 8, st);
-        a.trace = tr;
-        g_ilu_trace = tr;
-        g_ilu_trace_n = trn;
-    }
-#endif
     int rc;
     switch (g.r) {
         case 1: rc = launch3<1>(a, st); break;
