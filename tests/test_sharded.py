@@ -553,3 +553,29 @@ def test_comm_abi_one_rank_nccl():
             lib.lp_comm_destroy(h)
         nccl.ncclCommDestroy.argtypes = [ctypes.c_void_p]
         nccl.ncclCommDestroy(comm)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,N,T", [("cfg5", 18, 2), ("cfg4", 14, 8)])
+def test_rank_ilu0_one_rank_nccl_bitwise(name, N, T):
+    """ilu0_rank -- the per-process entry of the multi-GPU factorisation (factor
+    and flag arrays in CUDA-IPC memory, handle exchange, lp_ilu0_rank_prepare,
+    barrier, lp_ilu0_rank) -- as a one-rank NCCL job reproduces the single-GPU
+    factors bit for bit, and the solve with them is the single-GPU solve."""
+    import torch.distributed as dist
+    from paper_2004_13961_b200 import ProblemSpec, TransformPlan, assemble_M, ilu0, precond_apply
+    from paper_2004_13961_b200.sharded import ilu0_rank
+    w = wl.CONFIGS[name]()
+    spec = ProblemSpec(dim=3, N=N, beta=w.beta, alpha=w.alpha)
+    plan = TransformPlan(N + 1)
+    ref = ilu0(assemble_M(spec, T, T, plan))
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0,
+                            world_size=1)
+    try:
+        fac = ilu0_rank(assemble_M(spec, T, T, plan), 0, 1)
+    finally:
+        dist.destroy_process_group()
+    np.testing.assert_array_equal(fac.L.values, ref.L.values)
+    np.testing.assert_array_equal(fac.U.values, ref.U.values)
+    r = np.random.default_rng(2).standard_normal(ref.n)
+    np.testing.assert_array_equal(precond_apply(fac, r), precond_apply(ref, r))
