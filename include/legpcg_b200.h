@@ -248,14 +248,15 @@ int lp_pcg_solve(lp_operator *op, lp_ilu *precond, const double *F, double *x,
 
 /* --------------------------------------------------------- vector ops --
  * Building blocks exposed for tests and for host-driven loops. */
-/* out[0..1] (device) = double-double sum_i a_i b_i, deterministic order. */
-/* PCG vector updates with host scalars (sharded driver, sharded.py):
- * p = z (first != 0) or z + beta p;  x += alpha p, r -= alpha w with the
- * double-double r'r of the slab in out2[0..1] (device). */
+/* _dot (pcg.py:77-79): out2[0..1] (device) = double-double sum_i a_i b_i in a
+ * fixed order (bitwise reproducible for a given n). */
+int lp_dot(int64_t n, const double *a, const double *b, double *out2, void *stream);
+/* PCG vector updates (pcg.py:150-155,161-162) with host scalars (sharded driver,
+ * sharded.py): p = z (first != 0) or z + beta p;  x += alpha p, r -= alpha w
+ * with the double-double r'r of the slab in out2[0..1] (device). */
 int lp_update_p(int64_t n, const double *z, double *p, double beta, int first, void *stream);
 int lp_update_xr(int64_t n, double *x, double *r, const double *p, const double *w, double alpha,
                  double *out2, void *stream);
-int lp_dot(int64_t n, const double *a, const double *b, double *out2, void *stream);
 
 /* ------------------------------------------------------------ multi-GPU --
  * Collectives of the distributed solve on the caller's NCCL communicator
