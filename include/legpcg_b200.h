@@ -84,6 +84,12 @@ int lp_operator_destroy(lp_operator *op);
 /* which: 1 = A (apply_A), 2 = B (apply_B), 3 = A + B (apply_system).
  * u, out: device, K^d, x fastest.  out may not alias u. */
 int lp_apply(lp_operator *op, int which, const double *u, double *out, void *stream);
+/* The same with the scalar u'(Op u) as a second output (the curvature p'w of
+ * pcg.py:156-157): uw points to two device doubles (a double-double pair).
+ * The last line pass of the matvec accumulates it in its epilogue, one part
+ * per CTA, summed in double-double in a fixed order (deterministic). */
+int lp_apply_dot(lp_operator *op, int which, const double *u, double *out, double *uw,
+                 void *stream);
 
 /* ------------------------------------------------ slab-sharded 3-D matvec --
  * apply_system (operator.py:204-210) split into the compute stages of a

@@ -51,6 +51,7 @@ _SIGS = {
                                   ctypes.POINTER(_vp)]),
     "lp_operator_destroy": (_i32, [_vp]),
     "lp_apply": (_i32, [_vp, _i32, _vp, _vp, _vp]),
+    "lp_apply_dot": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp]),
     "lp_csr_create": (_i32, [_i64, _i64, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
     "lp_box_assemble": (_i32, [_i32, _i32, _i32, _vp, _vp, ctypes.POINTER(_vp), _i32, _vp,
                                ctypes.POINTER(_vp)]),

@@ -208,6 +208,7 @@ line_transform_kernel(const __grid_constant__ LtArgs a) {
                 }
         }
     }
+    double pw = 0.0;   // this thread's part of the fused dot (FOLD, a.dotv)
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -236,6 +237,10 @@ line_transform_kernel(const __grid_constant__ LtArgs a) {
                         const int k0 = 2 * row;
                         if (k0 < a.nk) o.out[(size_t)k0 * a.B + b] = x0;
                         if (k0 + 1 < a.nk) o.out[(size_t)(k0 + 1) * a.B + b] = x1;
+                        if (a.dotv) {
+                            if (k0 < a.nk) pw = fma(x0, __ldg(a.dotv + (size_t)k0 * a.B + b), pw);
+                            if (k0 + 1 < a.nk) pw = fma(x1, __ldg(a.dotv + (size_t)(k0 + 1) * a.B + b), pw);
+                        }
                     }
                 }
         }
@@ -244,6 +249,20 @@ line_transform_kernel(const __grid_constant__ LtArgs a) {
         if (b < a.B) {
             const size_t idx = (size_t)a.mid * a.B + b;
             o.out[idx] = o.grid ? midacc * __ldg(o.grid + idx) : midacc;
+        }
+    }
+    if (a.dotv) {
+        // the CTA's sum in a fixed order: xor butterfly per warp, the warps in order
+#pragma unroll
+        for (int s = 16; s; s >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, s);
+        __syncthreads();   // the tile buffers are free
+        if (lane == 0) smem[warp] = pw;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int w8 = 0; w8 < THREADS / 32; ++w8) t += smem[w8];
+            a.dotpart[blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z)] = t;
         }
     }
 }
@@ -367,6 +386,10 @@ void lt_set_out(LtArgs &a, int oi, double *out, const double *grid) {
     a.outs[oi].out = out;
     a.outs[oi].grid = grid;
     if (oi + 1 > a.nouts) a.nouts = oi + 1;
+}
+
+int64_t line_transform_ctas(const LtArgs &a) {
+    return ceil_div(a.B, BN) * (int64_t)(a.Mdim / BM) * a.nouts;
 }
 
 int line_transform(const LtArgs &a, cudaStream_t st) {

@@ -66,6 +66,11 @@ struct LtArgs {
     int Mdim, Kdim;    // GEMM extents (unpadded): UNFOLD Hm x max(KE,KO); FOLD max(KE,KO) x Hm
     int nouts;
     LtOut outs[4];
+    // FOLD passes with one output: dotpart[cta] = sum over the CTA's output tile of
+    // out * dotv (same indexing as out) -- the p'w of pcg.py:157 inside the last
+    // pass of the matvec; one value per CTA in a fixed order.  Null: no dot.
+    const double *dotv;
+    double *dotpart;
 };
 
 int line_table_build(LineTable &t, const double *Tdev, int P, int nk, int ps,
@@ -74,6 +79,8 @@ void line_table_free(LineTable &t);
 
 // Launch one pass.  Terms must all share the table shape of `shape`.
 int line_transform(const LtArgs &a, cudaStream_t st);
+// CTAs of that launch (the length of dotpart)
+int64_t line_transform_ctas(const LtArgs &a);
 
 // Helpers to fill LtArgs from tables.
 LtArgs lt_unfold(const LineTable &shape, int B);

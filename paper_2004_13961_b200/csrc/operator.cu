@@ -15,6 +15,7 @@
 
 #include "line_transform.cuh"
 #include "operator.cuh"
+#include "vector_ops.cuh"
 
 namespace lp {
 namespace {
@@ -294,24 +295,32 @@ extern "C" int lp_operator_destroy(lp_operator *op) {
 
 namespace lp {
 
-int64_t operator_ws_doubles(const lp_operator *op) { return 7 * op->nP; }
+// 7 fields of P^d plus the per-CTA parts of the fused p'w (last fold pass: at most
+// ceil(K^(d-1) / 64) * ceil(K / 128) CTAs)
+static int64_t dot_parts(const lp_operator *op) {
+    const int64_t lines = ipow(op->K, op->d - 1);
+    return ((lines + LT_BN - 1) / LT_BN) * ((op->K / 2 + 1 + LT_BM - 1) / LT_BM + 1);
+}
+int64_t operator_ws_doubles(const lp_operator *op) { return 7 * op->nP + dot_parts(op); }
 
 static int operator_apply_ws(lp_operator *op, int which, const double *u, double *out,
-                             cudaStream_t st, double *ws);
+                             cudaStream_t st, double *ws, double *uw);
 
 int operator_apply(lp_operator *op, int which, const double *u, double *out, cudaStream_t st,
-                   double *ws) {
-    if (ws) return operator_apply_ws(op, which, u, out, st, ws);
+                   double *ws, double *uw) {
+    if (ws) return operator_apply_ws(op, which, u, out, st, ws, uw);
     double *tmp = nullptr;
     int rc = salloc(&tmp, (size_t)operator_ws_doubles(op), "operator workspace", st);
     if (rc) return rc;
-    rc = operator_apply_ws(op, which, u, out, st, tmp);
+    rc = operator_apply_ws(op, which, u, out, st, tmp, uw);
     sfree(tmp, st);
     return rc;
 }
 
+// uw (optional, device double-double pair): u' out, accumulated by the last fold
+// pass (a part per CTA, summed in double-double in a fixed order).
 static int operator_apply_ws(lp_operator *op, int which, const double *u, double *out,
-                             cudaStream_t st, double *ws) {
+                             cudaStream_t st, double *ws, double *uw) {
     const lp_plan *pl = op->plan;
     const LineTable &F = pl->tPhi, &D = pl->tDPhi;
     const int K = op->K, P = op->P, d = op->d;
@@ -324,9 +333,21 @@ static int operator_apply_ws(lp_operator *op, int which, const double *u, double
     const int64_t nK = ipow(K, d);
     if (!hasA && !hasB) {
         LP_CUDA(cudaMemsetAsync(out, 0, nK * sizeof(double), st));
+        if (uw) LP_CUDA(cudaMemsetAsync(uw, 0, 2 * sizeof(double), st));
         return LP_OK;
     }
     int rc;
+    double *parts = ws + 7 * nP;
+    int64_t nparts = 0;
+#define LAST(args)                                                    \
+    do {                                                              \
+        if (uw) {                                                     \
+            (args).dotv = u;                                          \
+            (args).dotpart = parts;                                   \
+            nparts = line_transform_ctas(args);                       \
+        }                                                             \
+        if ((rc = line_transform((args), st))) return rc;             \
+    } while (0)
 #define RUN(args)                                   \
     do {                                            \
         if ((rc = line_transform((args), st))) return rc; \
@@ -341,7 +362,7 @@ static int operator_apply_ws(lp_operator *op, int which, const double *u, double
         if (hasA) lt_add_term(f, 0, D, A[0]);
         if (hasB) lt_add_term(f, 0, F, A[1]);
         lt_set_out(f, 0, out);
-        RUN(f);
+        LAST(f);
     } else if (d == 2) {
         // S1 along x: G0 = Phi u (A[0]), G1 = dPhi u (A[1]) -> [x'][y]
         LtArgs s1 = lt_unfold(F, K);
@@ -371,7 +392,7 @@ static int operator_apply_ws(lp_operator *op, int which, const double *u, double
         lt_add_term(s4, 0, F, A[0]);
         if (hasA) lt_add_term(s4, 0, D, A[1]);
         lt_set_out(s4, 0, out);
-        RUN(s4);
+        LAST(s4);
     } else {
         // S1 along x: Gx0 = Phi u (A0), Gx1 = dPhi u (A1) -> [x'][z][y]
         LtArgs s1 = lt_unfold(F, K * K);
@@ -421,13 +442,29 @@ static int operator_apply_ws(lp_operator *op, int which, const double *u, double
         lt_add_term(b3, 0, F, A[0]);
         if (hasA) lt_add_term(b3, 0, D, A[1]);
         lt_set_out(b3, 0, out);
-        RUN(b3);
+        LAST(b3);
     }
 #undef RUN
+#undef LAST
+    if (uw) {
+        if (nparts > dot_parts(op)) {
+            set_error("internal: %lld dot parts exceed the workspace", (long long)nparts);
+            return LP_ERR_ARG;
+        }
+        return sum_lines_dd(parts, nparts, uw, st);
+    }
     return LP_OK;
 }
 
 }  // namespace lp
+
+extern "C" int lp_apply_dot(lp_operator *op, int which, const double *u, double *out, double *uw,
+                            void *stream) {
+    LP_ARG(which >= 1 && which <= 3, "which must be 1 (A), 2 (B) or 3 (A+B)");
+    LP_ARG(u != out, "output may not alias the input");
+    LP_ARG(uw != nullptr, "uw must point to two device doubles");
+    return lp::operator_apply(op, which, u, out, as_stream(stream), nullptr, uw);
+}
 
 extern "C" int lp_apply(lp_operator *op, int which, const double *u, double *out, void *stream) {
     LP_ARG(which >= 1 && which <= 3, "which must be 1 (A), 2 (B) or 3 (A+B)");

@@ -36,6 +36,8 @@ int64_t operator_ws_doubles(const lp_operator *op);
 // apply_A / apply_B / apply_system.  ws: operator_ws_doubles(op) doubles of
 // device workspace, or null to take stream-ordered scratch for this call (the
 // handle is never written, so concurrent applies on different streams are safe).
+// uw (optional): device double-double pair receiving u' out (the p'w of pcg.py:157),
+// accumulated inside the last pass.
 int operator_apply(lp_operator *op, int which, const double *u, double *out, cudaStream_t st,
-                   double *ws = nullptr);
+                   double *ws = nullptr, double *uw = nullptr);
 }

@@ -101,8 +101,8 @@ int iteration(const Loop &L, int64_t it, cudaStream_t st) {
         return rc;
     }
     if ((rc = pcg_update_p(L.n, zz, ws.p, rho_new, rho_old, it == 1, st))) return rc;
-    if ((rc = operator_apply(L.op, 3, ws.p, ws.w, st, ws.opws))) return rc;
-    if ((rc = dot_dd(L.n, ws.p, ws.w, ws.partial, sc + S_CURV, st))) return rc;
+    // w = (A + B) p with the curvature p'w carried by the last pass (pcg.py:156-157)
+    if ((rc = operator_apply(L.op, 3, ws.p, ws.w, st, ws.opws, sc + S_CURV))) return rc;
     if ((rc = pcg_update_xr(L.n, L.x, ws.r, ws.p, ws.w, rho_new, sc + S_CURV, ws.partial, st)))
         return rc;
     if ((rc = finalize_dd(ws.partial, sc + S_RR, st))) return rc;

@@ -206,6 +206,18 @@ def apply_flat(spec, plan, which, u_flat):
     return out
 
 
+def apply_flat_dot(spec, plan, which, u_flat):
+    """(out, u'out): the matvec with the PCG curvature p'w (pcg.py:156-157)
+    accumulated inside its last pass (``lp_apply_dot``; double-double,
+    deterministic).  Device x-fastest vector in, device vector and float out."""
+    out = device.empty(u_flat.numel())
+    uw = device.empty(2)
+    _lib.check(_lib.load().lp_apply_dot(spec.device_operator(plan), which, u_flat.data_ptr(),
+                                        out.data_ptr(), uw.data_ptr(), _lib.stream_ptr()), "apply")
+    hi, lo = (float(v) for v in device.host(uw))
+    return out, hi + lo
+
+
 def _apply(spec, plan, u, which):
     _check_input(spec, plan, u)
     dev_in = device.is_device(u.data)

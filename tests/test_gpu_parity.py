@@ -436,3 +436,25 @@ def test_precond_apply_rz_fused(name, N, T):
     assert abs(rz - ref) <= 1e-13 * scale
     z2, rz2 = precond_apply_rz(f, r)
     assert rz2 == rz
+
+
+@pytest.mark.parametrize("name,N", [("cfg1", 128), ("cfg2", 64), ("cfg2", 256), ("cfg3", 300), ("cfg4", 20),
+                                    ("cfg5", 40)])
+def test_apply_dot_fused(name, N):
+    """lp_apply_dot: the same w as lp_apply bit for bit, and u'w (accumulated in
+    the last line pass, pcg.py:156-157) within 1e-13 of the long-double dot;
+    deterministic."""
+    from paper_2004_13961_b200 import device
+    from paper_2004_13961_b200.operator import apply_flat, apply_flat_dot
+    w = wl.CONFIGS[name]()
+    spec = spec_of(w, N)
+    plan = TransformPlan(N + 1)
+    u = device.to_device(np.random.default_rng(4).standard_normal(spec.n_modes ** w.dim))
+    ref = apply_flat(spec, plan, 3, u)
+    out, uw = apply_flat_dot(spec, plan, 3, u)
+    assert bool((out == ref).all())
+    uh, wh = device.host(u).astype(np.longdouble), device.host(ref).astype(np.longdouble)
+    exact = float(np.dot(uh, wh))
+    scale = float(np.dot(np.abs(uh), np.abs(wh)))
+    assert abs(uw - exact) <= 1e-13 * scale
+    assert apply_flat_dot(spec, plan, 3, u)[1] == uw
