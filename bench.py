@@ -351,7 +351,9 @@ def run_b200(args, ws, rank, local):
     F_ilu = 2.0 * upd * n if upd else None
     ilu_tf = F_ilu / t_fac / 1e12 if F_ilu else None
     roof_fac = {"kernel": "ilu2d_kernel (2-D block wavefront)" if w.dim == 2 else "box_ilu0_3d_kernel",
-                "bound": "fp64 (separately rounded mul + sub, bitwise reference order)",
+                "bound": "fp64 (separately rounded mul + sub, bitwise reference order: vector pipe, no "
+                         "FMA and no tensor cores -- its own ceiling is 18.6 TFLOP/s, measured by "
+                         "scripts/micro/fp64_tput.cu; frac is against the DGEMM peak)",
                 "achieved": ilu_tf, "peak": fp64, "unit": "TFLOP/s",
                 "frac": ilu_tf / fp64 if ilu_tf else None,
                 "traffic": ncu_traffic(w.name, "ilu", 1), "algorithmic_flops": F_ilu,
